@@ -1,0 +1,281 @@
+/*
+ * lp_b200.h — C-ABI of the B200-native Latent Parallelism (LP) engine.
+ *
+ * This is the drop-in boundary for the reference's (lpsim) hot path: the
+ * per-step partition / denoise / reconstruct / sampler loop of
+ * /root/reference/proj/src/cluster.cpp:166-225.  Every entry point below names
+ * the reference interface it replaces (file:line, paths relative to
+ * /root/reference/proj).  Plain C types only: pointers, sizes, POD structs.
+ *
+ * Conventions
+ *  - Return value is a status: 0 = OK, otherwise (lpsim::ErrorKind + 1), see
+ *    lp_status (include/lpsim/errors.hpp:10-24), or LP_ERR_CUDA / LP_ERR_NCCL.
+ *    lp_last_error() returns a thread-local message for the last failure.
+ *  - Storage dtypes use the reference's byte codes (include/lpsim/dtype.hpp:10-14):
+ *    2 = IEEE binary16, 4 = binary32, 8 = binary64.  Device buffers hold exactly
+ *    the bits the reference's quantized doubles represent.
+ *  - Latents are dense row-major (c, t, h, w), channel outermost
+ *    (include/lpsim/latent.hpp:90-92).
+ *  - All device pointers are caller-owned; stream-ordered calls never allocate
+ *    and never synchronize the host.  `stream` is a cudaStream_t passed as void*.
+ *  - There is no CPU fallback: device calls fail with LP_ERR_CUDA when no
+ *    sm_100a device is present.
+ */
+#ifndef LP_B200_H
+#define LP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: lpsim::ErrorKind + 1 (include/lpsim/errors.hpp:10-24) ---- */
+enum lp_status {
+    LP_OK = 0,
+    LP_ERR_OUT_OF_BOUNDS = 1,
+    LP_ERR_EMPTY_RANGE = 2,
+    LP_ERR_DEGENERATE_AXIS = 3,
+    LP_ERR_INVALID_OVERLAP_RATIO = 4,
+    LP_ERR_OUTSIDE_EXTENT = 5,
+    LP_ERR_ZERO_WEIGHT = 6,
+    LP_ERR_SHAPE_MISMATCH = 7,
+    LP_ERR_WORKER_FAILURE = 8,
+    LP_ERR_INVALID_GROUPING = 9,
+    LP_ERR_INVALID_ARGUMENT = 10,
+    LP_ERR_NON_FINITE = 11,
+    LP_ERR_CONFIG = 12,
+    LP_ERR_IO = 13,
+    LP_ERR_CUDA = 100,
+    LP_ERR_NCCL = 101
+};
+
+/* Axis order = rotation order (include/lpsim/latent.hpp:17-24). */
+enum lp_axis { LP_AXIS_T = 0, LP_AXIS_H = 1, LP_AXIS_W = 2 };
+
+/* Reconstruct+update arithmetic (K10).  EXACT reproduces the reference's fp64,
+ * worker-ordered, non-fused arithmetic bit for bit; FAST accumulates in fp32. */
+enum lp_mode { LP_MODE_EXACT = 0, LP_MODE_FAST = 1 };
+
+/* Toy denoisers (src/denoise.cpp:56-142), used as bit-exact parity fixtures. */
+enum lp_toy_kind { LP_TOY_BOX = 0, LP_TOY_GLOBAL = 1, LP_TOY_IDENTITY = 2 };
+
+#define LP_MAX_WORKERS 256
+
+/* One worker's assignment — PartitionEntry (include/lpsim/partition.hpp:22-30). */
+typedef struct lp_entry {
+    int32_t worker_id; /* k, 1-based */
+    int32_t reserved;
+    int64_t core_begin, core_end;     /* core_patches   */
+    int64_t ext_begin, ext_end;       /* ext_patches    */
+    int64_t latent_begin, latent_end; /* latent [s, e) */
+    int64_t delta_start, delta_end;   /* Δs, Δe (latent units) */
+} lp_entry;
+
+/* PartitionPlan (include/lpsim/partition.hpp:32-46). */
+typedef struct lp_plan {
+    int32_t axis;       /* lp_axis */
+    int32_t step_index; /* i, 1-based */
+    double overlap_ratio;
+    int64_t patches_per_core; /* L */
+    int64_t overlap_patches;  /* O */
+    int64_t axis_patches;     /* N */
+    int64_t axis_extent;      /* D */
+    int64_t patch_size;       /* p */
+    int32_t n_entries;        /* K_eff */
+    int32_t reserved;
+    lp_entry entries[LP_MAX_WORKERS];
+} lp_plan;
+
+/* ------------------------------------------------------------------------ */
+/* Diagnostics                                                              */
+/* ------------------------------------------------------------------------ */
+const char* lp_last_error(void);
+const char* lp_version(void);
+/* Warning sink — set_warning_handler (include/lpsim/partition.hpp:48-52,
+ * src/partition.cpp:13-28).  NULL handler silences; the default prints to stderr. */
+typedef void (*lp_warning_fn)(const char* message, void* user);
+void lp_set_warning_handler(lp_warning_fn fn, void* user);
+
+/* ------------------------------------------------------------------------ */
+/* Host-side plan builder (bit-exact with src/partition.cpp:38-134)         */
+/* ------------------------------------------------------------------------ */
+/* rotation_axis — src/partition.cpp:38-43 */
+int lp_rotation_axis(int step_index, int32_t* axis_out);
+/* core_bounds — src/partition.cpp:45-62; out = 2*K int64 [begin,end) pairs */
+int lp_core_bounds(int64_t patches, int workers, int64_t* ranges_out, int32_t* n_out);
+/* extend_overlap — src/partition.cpp:64-78 */
+int lp_extend_overlap(const int64_t* cores, int32_t n_cores, int64_t patches, int64_t patches_per_core,
+                      double overlap_ratio, int workers, int64_t* ext_out);
+/* build_axis_plan — src/partition.cpp:80-123 */
+int lp_build_axis_plan(int32_t axis, int64_t axis_extent, int64_t axis_patch, int step_index, int workers,
+                       double overlap_ratio, lp_plan* plan_out);
+/* build_plan_for_shape — src/partition.cpp:125-129; shape = {c,t,h,w}, patch = {p_t,p_h,p_w} */
+int lp_build_plan(const int64_t shape[4], const int64_t patch[3], int step_index, int workers,
+                  double overlap_ratio, lp_plan* plan_out);
+/* build_weight_mask — src/reconstruct.cpp:9-27; out has latent_end-latent_begin doubles */
+int lp_weight_profile(const lp_plan* plan, int32_t entry, double* profile_out);
+/* Elements of entry k's sub-latent, and the packed (worker-ordered) offsets of all
+ * entries: offsets_out has n_entries+1 values (the gather buffer layout). */
+int lp_plan_offsets(const lp_plan* plan, const int64_t shape[4], int64_t* offsets_out);
+
+/* Multi-rank shard layout: entries are assigned to ranks round-robin
+ * (entry e -> rank e % world).  For `rank`, writes the entry ids it owns
+ * (owned_out, up to LP_MAX_WORKERS) and their count; slot_elems_out = the
+ * padded per-rank slot of the all-gather buffer (max over ranks of the summed
+ * elements it owns).  Rank r's slot holds its entries packed in worker order. */
+int lp_shard_layout(const lp_plan* plan, const int64_t shape[4], int world, int rank, int32_t* owned_out,
+                    int32_t* n_owned_out, int64_t* slot_elems_out);
+
+/* Communication accounting — CommLedger + run_lp metering (src/cluster.cpp:27-73,
+ * 186-209): the reference ledger bytes of step i (2 passes x (scatter+gather)
+ * x sum_{k>=2} S_sub x wire_bytes), and the bytes this engine's padded all-gather
+ * receives on all ranks together (world-1 foreign slots per rank x slot x dtype). */
+int lp_step_comm_bytes(const lp_plan* plan, const int64_t shape[4], int wire_bytes, int world, int dtype_bytes,
+                       uint64_t* ledger_bytes_out, uint64_t* allgather_bytes_out);
+
+/* Quantizer (src/dtype.cpp:34-116), host side, for tests and host shims. */
+uint16_t lp_f16_encode(double v);
+double lp_f16_decode(uint16_t bits);
+double lp_quantize(double v, int dtype_bytes);
+
+/* ------------------------------------------------------------------------ */
+/* Device kernels (stream-ordered; sm_100a)                                  */
+/* ------------------------------------------------------------------------ */
+/* Device + context management.  A context binds one CUDA device. */
+int lp_device_check(int device); /* LP_OK iff device exists and is sm_100 */
+
+/* K1: partition gather — extract_sublatents / slice_axis
+ * (src/partition.cpp:136-148, src/latent.cpp:81-111).  Copies the entries
+ * [first, first+count) of `plan` from z into `dst`, packed in worker order
+ * (entry first at dst[0], next at dst[size(first)], ...).  Bit-exact copy. */
+int lp_extract(const lp_plan* plan, int32_t first, int32_t count, const void* z, const int64_t shape[4],
+               int dtype_bytes, void* dst, void* stream);
+
+/* K11: toy denoisers — Denoiser::predict of Box/GlobalMix/Identity
+ * (src/denoise.cpp:56-142).  `cond_mean` = ConditioningVector::mean()
+ * (src/denoise.cpp:17-22).  fp64, the reference's summation order. */
+int lp_toy_predict(int32_t kind, const int64_t radius[3], double t_coeff, double cond_coeff, const void* z,
+                   const int64_t shape[4], int dtype_bytes, int timestep, double cond_mean, void* out,
+                   void* stream);
+/* cfg_predict with a toy denoiser (src/denoise.cpp:24-39), fused: one pass
+ * computes uncond (null cond, mean 0) and cond predictions, each quantized,
+ * then uncond + w*(cond-uncond) in fp64, quantized.  `workspace` needs
+ * lp_toy_workspace_bytes(shape) bytes (GlobalMix channel sums), else NULL. */
+int lp_toy_cfg_predict(int32_t kind, const int64_t radius[3], double t_coeff, double cond_coeff, const void* z,
+                       const int64_t shape[4], int dtype_bytes, int timestep, double cond_mean, double guidance,
+                       void* eps_out, void* workspace, void* stream);
+size_t lp_toy_workspace_bytes(const int64_t shape[4]);
+
+/* CFG combine of two already-quantized predictions (src/denoise.cpp:34-38). */
+int lp_cfg_combine(const void* uncond, const void* cond, int64_t n, int dtype_bytes, double guidance, void* out,
+                   void* stream);
+
+/* reconstruct (src/reconstruct.cpp:42-121): `preds` = all entries' predictions
+ * packed in worker order (layout of lp_plan_offsets).  Writes ε̂ (quantized). */
+int lp_reconstruct(const lp_plan* plan, const void* preds, const int64_t shape[4], int dtype_bytes, int32_t mode,
+                   void* eps_out, void* stream);
+/* sampler_step (src/denoise.cpp:41-52): z_out = quantize(z - eta*eps). */
+int lp_sampler_step(const void* z, const void* eps, int64_t n, int dtype_bytes, double eta, void* z_out,
+                    void* stream);
+/* K10: reconstruct + sampler_step fused, in place on z (one HBM pass):
+ * z = quantize(z - eta * quantize(Σ_k w_k·pred_k / Σ_k w_k)). */
+int lp_reconstruct_update(const lp_plan* plan, const void* preds, const int64_t shape[4], int dtype_bytes,
+                          int32_t mode, double eta, void* z, void* stream);
+
+/* Synthetic inputs — synthetic_inputs (src/run_config.cpp:258-301), host side:
+ * mt19937_64 + pinned Box-Muller; latent quantized to dtype, 8 cond values. */
+int lp_synthetic_inputs(const int64_t shape[4], int dtype_bytes, uint64_t seed, double* latent_out,
+                        double* cond_out8);
+
+/* ------------------------------------------------------------------------ */
+/* DiT denoiser (the plugin slot Denoiser::predict, include/lpsim/denoise.hpp:31-39) */
+/* ------------------------------------------------------------------------ */
+typedef struct lp_dit_config {
+    int32_t in_channels;  /* 16 */
+    int32_t dim;          /* 1536 (1.3B) / 5120 (14B) */
+    int32_t ffn_dim;      /* 8960 / 13824 */
+    int32_t num_heads;    /* 12 / 40 ; head_dim = dim/num_heads = 128 */
+    int32_t num_layers;   /* 30 / 40 */
+    int32_t text_len;     /* 512 */
+    int32_t text_dim;     /* 4096 */
+    int32_t freq_dim;     /* 256 */
+    int32_t patch[3];     /* 1,2,2 */
+    int32_t reserved;
+    double eps;           /* LayerNorm / RMSNorm eps, 1e-6 */
+    double t_scale;       /* sinusoid input = t * t_scale (builder-pinned; 1000/T) */
+    uint64_t seed;        /* weights + synthetic text context */
+} lp_dit_config;
+
+typedef struct lp_dit lp_dit;
+
+void lp_dit_default_config(lp_dit_config* cfg); /* WAN2.1-1.3B shape */
+/* Allocates weights (bf16) and the cond/uncond text K/V caches on the current
+ * device, initialised from the pinned generator (see lp_dit_param). */
+int lp_dit_create(const lp_dit_config* cfg, const double* cond_values, int32_t n_cond, lp_dit** out);
+int lp_dit_destroy(lp_dit* dit);
+/* Workspace for shards up to max_tokens tokens (allocates; call once). */
+int lp_dit_reserve(lp_dit* dit, int64_t max_tokens);
+/* cfg_predict with the DiT: CFG batch 2 (uncond = null text, cond = synthetic
+ * text), one forward, combine uncond + w*(cond-uncond), quantize to dtype. */
+int lp_dit_cfg_predict(lp_dit* dit, const void* sub, const int64_t shape[4], int dtype_bytes, int timestep,
+                       double guidance, void* eps_out, void* stream);
+/* Parameter access for tests: index -> name, device pointer, element count, dtype (2=bf16,4=f32). */
+int lp_dit_num_params(const lp_dit* dit);
+int lp_dit_param(const lp_dit* dit, int32_t index, const char** name, void** dptr, int64_t* numel,
+                 int32_t* elem_bytes);
+/* Intermediate-tensor access for per-block tests (valid after a forward). */
+int lp_dit_debug_tensor(const lp_dit* dit, const char* name, void** dptr, int64_t* numel);
+
+/* ------------------------------------------------------------------------ */
+/* Standalone GEMM (tcgen05) — exposed for unit tests and the bench roofline */
+/* ------------------------------------------------------------------------ */
+/* D[M,N] (bf16, row-major) = A[M,K] (bf16, row-major) · B[N,K]^T (bf16) + bias[N] (f32 or NULL). */
+int lp_gemm_bf16(const void* A, const void* B, const void* bias, void* D, int64_t M, int64_t N, int64_t K,
+                 void* stream);
+/* Flash attention forward (tcgen05): q,k,v,o bf16 [B, S, H, 128] row-major. */
+int lp_attention_bf16(const void* q, const void* k, const void* v, void* o, int64_t batch, int64_t seq_q,
+                      int64_t seq_kv, int64_t heads, double scale, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* LP engine: the run_lp step loop (src/cluster.cpp:166-225)                */
+/* ------------------------------------------------------------------------ */
+typedef struct lp_engine_config {
+    int64_t shape[4];
+    int64_t patch[3];
+    int32_t dtype_bytes;
+    int32_t workers;       /* K */
+    double overlap_ratio;  /* r */
+    int32_t total_steps;   /* T */
+    int32_t mode;          /* lp_mode for K10 */
+    double eta;
+    double guidance;
+    int32_t denoiser;      /* -1 = DiT (dit != NULL), else lp_toy_kind */
+    int32_t wire_bytes;    /* preset dtype_bytes for the reference ledger (2 = wan21-like) */
+    int64_t radius[3];
+    double t_coeff, cond_coeff;
+    int32_t world, rank;   /* ranks sharing the plan; entries round-robin over ranks */
+    lp_dit* dit;
+} lp_engine_config;
+
+typedef struct lp_engine lp_engine;
+
+/* NCCL plumbing for world > 1: rank 0 gets an id, the caller broadcasts it. */
+int lp_nccl_unique_id(uint8_t id_out[128]);
+int lp_engine_create(const lp_engine_config* cfg, const uint8_t* nccl_id, const double* cond, int32_t n_cond,
+                     lp_engine** out);
+int lp_engine_destroy(lp_engine* e);
+/* Device latent z (replicated on every rank), size shape volume * dtype. */
+int lp_engine_latent(lp_engine* e, void** z_dptr);
+/* Runs steps [first, first+count) (1-based i; t = T+1-i) on `stream`. */
+int lp_engine_run(lp_engine* e, int32_t first_step, int32_t count, void* stream);
+/* Bytes this engine moved over NCCL so far, and the reference ledger bytes. */
+int lp_engine_comm(const lp_engine* e, uint64_t* nccl_bytes, uint64_t* ledger_bytes);
+/* Kernel launches issued by the engine so far (this library's kernels only). */
+int lp_engine_launches(const lp_engine* e, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LP_B200_H */

@@ -145,6 +145,11 @@ double lp_quantize(double v, int dtype_bytes);
 /* ------------------------------------------------------------------------ */
 /* Device + context management.  A context binds one CUDA device. */
 int lp_device_check(int device); /* LP_OK iff device exists and is sm_100 */
+/* Sticky device flags raised by kernels (1 = a stored value was non-finite:
+ * the reference's NonFinite, src/latent.cpp:72-77).  Synchronizes. */
+int lp_device_flags(uint32_t* flags_out, int reset);
+/* Kernel launches issued by this library since load. */
+uint64_t lp_launch_count(void);
 
 /* K1: partition gather — extract_sublatents / slice_axis
  * (src/partition.cpp:136-148, src/latent.cpp:81-111).  Copies the entries

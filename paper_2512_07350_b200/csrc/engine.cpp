@@ -1,0 +1,190 @@
+// engine.cpp — the run_lp step loop (src/cluster.cpp:166-225), B200-native.
+//
+// One engine per rank (one process per GPU).  Per step i (t = T+1-i):
+//   1. plan for rotation_axis(i) — precomputed on the host at creation (the plan
+//      depends only on the axis, src/partition.cpp:125-129), bit-exact;
+//   2. K1 gathers each OWNED entry's window from the replicated latent z
+//      (no scatter: every rank holds z);
+//   3. the denoiser runs cfg_predict on it (DiT: CFG batch 2 in one forward),
+//      writing ε̂_k straight into this rank's slot of the gather buffer;
+//   4. world > 1: ONE ncclAllGather of the padded slots (latent shards only,
+//      never DiT activations);
+//   5. K10 blends all entries in worker order and applies the sampler update to
+//      z in place, redundantly on every rank, so z stays replicated.
+// Entries are assigned round-robin (entry e -> rank e % world), so world = 1
+// runs all K workers' shards on one GPU ("K ranks on one GPU").
+#include <nccl.h>
+
+#include <cstring>
+#include <vector>
+
+#include "recon.hpp"
+
+using namespace lpb200;
+
+#define LP_NCCL(call)                                                                        \
+    do {                                                                                     \
+        ncclResult_t _r = (call);                                                            \
+        if (_r != ncclSuccess) fail(LP_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(_r)); \
+    } while (0)
+
+struct lp_engine {
+    lp_engine_config cfg{};
+    Shape4 shape;
+    std::vector<double> cond;
+    double cond_mean = 0.0;
+    lp_plan plans[3];
+    ShardLayout layout[3];
+    std::vector<i64> elems[3];
+    ReconParams recon[3];
+    void* z = nullptr;
+    void* gather = nullptr;
+    void* sub = nullptr;
+    double* ws = nullptr;
+    ncclComm_t comm = nullptr;
+    uint64_t nccl_bytes = 0, ledger_bytes = 0, launches = 0;
+};
+
+extern "C" {
+
+int lp_nccl_unique_id(uint8_t id_out[128]) {
+    return guard([&] {
+        ncclUniqueId id;
+        LP_NCCL(ncclGetUniqueId(&id));
+        static_assert(sizeof(id) == 128, "ncclUniqueId size");
+        std::memcpy(id_out, &id, 128);
+    });
+}
+
+int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const double* cond, int32_t n_cond,
+                     lp_engine** out) {
+    return guard([&] {
+        check_dtype(c->dtype_bytes);
+        if (c->total_steps < 1) fail(LP_ERR_INVALID_ARGUMENT, "total_steps must be >= 1");
+        if (c->workers < 1) fail(LP_ERR_INVALID_ARGUMENT, "cluster needs at least one worker");
+        if (c->wire_bytes != 2 && c->wire_bytes != 4 && c->wire_bytes != 8)
+            fail(LP_ERR_INVALID_ARGUMENT, "preset dtype_bytes must be 2, 4 or 8");
+        if (c->world < 1 || c->rank < 0 || c->rank >= c->world) fail(LP_ERR_INVALID_ARGUMENT, "bad world/rank");
+        if (c->denoiser < 0 && !c->dit) fail(LP_ERR_INVALID_ARGUMENT, "DiT engine without a DiT");
+        auto* e = new lp_engine();
+        e->cfg = *c;
+        e->shape = Shape4::from(c->shape);
+        e->cond.assign(cond, cond + n_cond);
+        if (n_cond > 0) {  // ConditioningVector::mean (src/denoise.cpp:17-22)
+            double acc = 0.0;
+            for (double v : e->cond) acc += v;
+            e->cond_mean = acc / static_cast<double>(n_cond);
+        }
+        try {
+            i64 max_slot = 0, max_entry = 0;
+            for (int a = 0; a < 3; ++a) {
+                // step index a+1 has axis a; step_index is cosmetic in the plan
+                e->plans[a] = build_plan_for_shape(e->shape, c->patch, a + 1, c->workers, c->overlap_ratio);
+                e->layout[a] = shard_layout(e->plans[a], e->shape, c->world, c->rank);
+                e->elems[a] = entry_elems(e->plans[a], e->shape);
+                e->recon[a] = make_recon_params(e->plans[a], e->shape, e->layout[a].base, c->eta);
+                max_slot = std::max(max_slot, e->layout[a].slot_elems);
+                for (i64 n : e->elems[a]) max_entry = std::max(max_entry, n);
+            }
+            const size_t E = static_cast<size_t>(c->dtype_bytes);
+            LP_CUDA(cudaMalloc(&e->z, static_cast<size_t>(e->shape.volume()) * E));
+            LP_CUDA(cudaMalloc(&e->gather, static_cast<size_t>(max_slot) * c->world * E));
+            LP_CUDA(cudaMemset(e->gather, 0, static_cast<size_t>(max_slot) * c->world * E));
+            LP_CUDA(cudaMalloc(&e->sub, static_cast<size_t>(max_entry) * E));
+            LP_CUDA(cudaMalloc(&e->ws, lp_toy_workspace_bytes(c->shape) + 64));
+            if (c->dit) {
+                // workspace for the largest shard the DiT will see (tokens per entry)
+                i64 max_tokens = 0;
+                for (int a = 0; a < 3; ++a)
+                    for (int k = 0; k < e->plans[a].n_entries; ++k) {
+                        const Shape4 s = e->shape.with_extent(a, e->plans[a].entries[k].latent_end -
+                                                                     e->plans[a].entries[k].latent_begin);
+                        max_tokens = std::max(max_tokens, (s.t / c->patch[0]) * (s.h / c->patch[1]) * (s.w / c->patch[2]));
+                    }
+                const int st = lp_dit_reserve(c->dit, max_tokens);
+                if (st) fail(st, lp_last_error());
+            }
+            if (c->world > 1) {
+                if (!nccl_id) fail(LP_ERR_INVALID_ARGUMENT, "world > 1 needs an NCCL unique id");
+                ncclUniqueId id;
+                std::memcpy(&id, nccl_id, 128);
+                LP_NCCL(ncclCommInitRank(&e->comm, c->world, id, c->rank));
+            }
+        } catch (...) {
+            lp_engine_destroy(e);
+            throw;
+        }
+        *out = e;
+    });
+}
+
+int lp_engine_destroy(lp_engine* e) {
+    if (!e) return LP_OK;
+    if (e->comm) ncclCommDestroy(e->comm);
+    cudaFree(e->z);
+    cudaFree(e->gather);
+    cudaFree(e->sub);
+    cudaFree(e->ws);
+    delete e;
+    return LP_OK;
+}
+
+int lp_engine_latent(lp_engine* e, void** z) {
+    *z = e->z;
+    return LP_OK;
+}
+
+int lp_engine_run(lp_engine* e, int32_t first, int32_t count, void* stream) {
+    return guard([&] {
+        const lp_engine_config& c = e->cfg;
+        cudaStream_t st = as_stream(stream);
+        const int E = c.dtype_bytes;
+        char* gather = static_cast<char*>(e->gather);
+        const uint64_t l0 = launch_count();
+        for (int i = first; i < first + count; ++i) {
+            if (i < 1 || i > c.total_steps) fail(LP_ERR_INVALID_ARGUMENT, "step out of range");
+            const int t = c.total_steps + 1 - i;
+            const int a = rotation_axis(i);
+            const lp_plan& plan = e->plans[a];
+            const ShardLayout& L = e->layout[a];
+            for (int k : L.owned) {
+                const lp_entry& en = plan.entries[k];
+                const Shape4 s = e->shape.with_extent(a, en.latent_end - en.latent_begin);
+                slice_to(e->z, e->shape, a, en.latent_begin, en.latent_end, E, e->sub, st);  // K1
+                void* eps = gather + static_cast<size_t>(L.base[k]) * E;
+                const int64_t sh[4] = {s.c, s.t, s.h, s.w};
+                int rc;
+                if (c.denoiser < 0)
+                    rc = lp_dit_cfg_predict(c.dit, e->sub, sh, E, t, c.guidance, eps, stream);
+                else
+                    rc = lp_toy_cfg_predict(c.denoiser, c.radius, c.t_coeff, c.cond_coeff, e->sub, sh, E, t,
+                                            e->cond_mean, c.guidance, eps, e->ws, stream);
+                if (rc) fail(LP_ERR_WORKER_FAILURE, "worker " + std::to_string(k + 1) + " failed at step " +
+                                                        std::to_string(i) + ": " + lp_last_error());
+            }
+            if (c.world > 1) {
+                const size_t slot = static_cast<size_t>(L.slot_elems) * E;
+                LP_NCCL(ncclAllGather(gather + slot * c.rank, gather, slot, ncclUint8, e->comm, st));
+                e->nccl_bytes += slot * static_cast<size_t>(c.world - 1);  // received by this rank
+            }
+            reconstruct_dispatch(e->recon[a], E, gather, e->z, nullptr, true, c.mode == LP_MODE_FAST, st);  // K10
+            uint64_t sum = 0;
+            for (size_t k = 1; k < e->elems[a].size(); ++k) sum += static_cast<uint64_t>(e->elems[a][k]);
+            e->ledger_bytes += 4ull * sum * static_cast<uint64_t>(c.wire_bytes);  // cluster.cpp:186-209
+        }
+        e->launches += launch_count() - l0;
+    });
+}
+
+int lp_engine_comm(const lp_engine* e, uint64_t* nccl_bytes, uint64_t* ledger_bytes) {
+    *nccl_bytes = e->nccl_bytes;
+    *ledger_bytes = e->ledger_bytes;
+    return LP_OK;
+}
+
+int lp_engine_launches(const lp_engine* e, uint64_t* launches) {
+    *launches = e->launches;
+    return LP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,27 @@
+// recon.hpp — K10 launch parameters (shared by lp_kernels.cu and engine.cpp).
+#pragma once
+#include <vector>
+
+#include "lp_host.hpp"
+
+namespace lpb200 {
+
+constexpr int kMaxKernelEntries = 64;
+// One plan entry as K10 sees it: latent window [begin, begin+len) with
+// ramps (ds, de) and the element offset of its prediction in the gather buffer.
+struct ReconEntry {
+    int64_t begin, len, ds, de, base;
+};
+struct ReconParams {
+    int n;
+    int64_t D, outer, inner, total;
+    double eta;
+    ReconEntry e[kMaxKernelEntries];
+};
+
+ReconParams make_recon_params(const lp_plan& plan, const Shape4& s, const std::vector<i64>& base, double eta);
+void reconstruct_dispatch(const ReconParams& p, int dtype, const void* preds, void* z, void* eps, bool update,
+                          bool fast, cudaStream_t st);
+void slice_to(const void* z, const Shape4& s, int axis, i64 begin, i64 end, int E, void* dst, cudaStream_t st);
+
+}  // namespace lpb200

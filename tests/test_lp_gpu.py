@@ -1,0 +1,147 @@
+"""GPU parity of the LP kernels (K1 gather, K10 reconstruct+sampler, K11 toy
+denoisers) and the engine loop against the CPU oracle — bit-exact (integer /
+byte work and the fp64 "exact" path)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle.oracle import sub_shape
+from paper_2512_07350_b200 import lp
+
+pytestmark = pytest.mark.gpu
+H = lambda a: hashlib.sha256(np.ascontiguousarray(a, np.float64).tobytes()).hexdigest()[:16]  # noqa: E731
+
+
+def _cases(seed, n):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        shape = tuple(int(v) for v in (rng.integers(1, 5), rng.integers(1, 14), rng.integers(1, 14), rng.integers(1, 14)))
+        patch = tuple(int(v) for v in rng.integers(1, 4, size=3))
+        k = int(rng.integers(1, 9))
+        r = float(min(rng.choice([0.0, 0.25, 0.5, 1.0, 1.5]), k - 1))
+        step = int(rng.integers(1, 4))
+        d = int(rng.choice([2, 4, 8]))
+        try:
+            lp.build_plan(shape, patch, step, k, r)
+        except lp.LpError:
+            continue
+        out.append((shape, patch, k, r, step, d, int(rng.integers(0, 1 << 30))))
+    return out
+
+
+def test_extract_bitexact(cuda, oracle):
+    for shape, patch, k, r, step, d, seed in _cases(1, 60):
+        z, _ = oracle.synthetic(shape, d, seed)
+        plan = lp.build_plan(shape, patch, step, k, r)
+        subs = lp.extract_sublatents(lp.LatentTensor.from_numpy(z, d), plan)
+        want = oracle.extract(z, oracle.build_plan(shape, patch, step, k, r))
+        got = np.concatenate([s.to_numpy().reshape(-1) for s in subs])
+        assert np.array_equal(got, want), (shape, patch, k, r, step, d)
+
+
+def test_toy_denoisers_bitexact(cuda, oracle):
+    for shape, patch, k, r, step, d, seed in _cases(2, 40):
+        z, cond = oracle.synthetic(shape, d, seed)
+        zt = lp.LatentTensor.from_numpy(z, d)
+        for kind, f in [(0, lp.BoxDenoiser((1, 2, 0))), (1, lp.GlobalMixDenoiser()), (2, lp.IdentityDenoiser())]:
+            radius = f.radius
+            t = 1 + seed % 50
+            got = lp.cfg_predict(f, zt, t, list(cond), 5.0).to_numpy()
+            want = oracle.cfg_predict(kind, radius, z, d, t, cond, 5.0)
+            assert np.array_equal(got, want), (kind, shape, d)
+            got = lp.denoiser_predict(f, zt, t, cond).to_numpy()
+            want = oracle.toy_predict(kind, radius, z, d, t, float(np.mean(cond)) if False else sum(cond) / 8,
+                                      t_coeff=f.t_coeff, cond_coeff=f.cond_coeff)
+            if kind == 2:
+                want = z
+            assert np.array_equal(got, want), (kind, shape, d)
+
+
+def test_reconstruct_and_update_bitexact(cuda, oracle):
+    for shape, patch, k, r, step, d, seed in _cases(3, 60):
+        z, cond = oracle.synthetic(shape, d, seed)
+        plan = lp.build_plan(shape, patch, step, k, r)
+        oplan = oracle.build_plan(shape, patch, step, k, r)
+        rng = np.random.default_rng(seed)
+        preds_np = [lp._quantize_np(rng.normal(size=sub_shape(shape, oplan, e)) * 3, d).astype(np.float64)
+                    for e in range(oplan.n)]
+        preds = [lp.LatentTensor.from_numpy(p, d) for p in preds_np]
+        packed = np.concatenate([p.reshape(-1) for p in preds_np])
+        want = oracle.reconstruct(packed, shape, d, oplan)
+        got = lp.reconstruct(preds, plan, shape).to_numpy()
+        assert np.array_equal(got, want), (shape, patch, k, r, step, d)
+        zt = lp.LatentTensor.from_numpy(z, d)
+        lp.reconstruct_update(preds, plan, zt, 0.05)
+        assert np.array_equal(zt.to_numpy(), oracle.sampler_step(z, want, d, 0.05))
+        fast = lp.reconstruct(preds, plan, shape, mode="fast").to_numpy()
+        tol = {2: 2e-3, 4: 2e-6, 8: 2e-6}[d]
+        np.testing.assert_allclose(fast, want, rtol=tol, atol=tol * 4)
+
+
+def test_sampler_bitexact(cuda, oracle):
+    for d in (2, 4, 8):
+        z, _ = oracle.synthetic((3, 5, 7, 9), d, 1)
+        e, _ = oracle.synthetic((3, 5, 7, 9), d, 2)
+        got = lp.sampler_step(lp.LatentTensor.from_numpy(z, d), lp.LatentTensor.from_numpy(e, d), 1, 0.1).to_numpy()
+        assert np.array_equal(got, oracle.sampler_step(z, e, d, 0.1))
+
+
+@pytest.mark.parametrize("d,hash_", [(4, "3ad2d84ae75b30e9"), (8, "e7cbc9b6807bca2e")])
+def test_engine_golden_crit1(cuda, d, hash_):
+    # crit-1 config: 4x12x16x16 seed 2025, box rho=2, K=2, r=1, 6 steps, eta .05, w 2, p=2
+    z, cond = lp.synthetic_latent((4, 12, 16, 16), d, 2025)
+    out, ledger = lp.run_lp("box", (2, 2, 2), z, 6, 0.05, 2.0, cond, (2, 2, 2), 2, 1.0)
+    assert H(out.to_numpy()) == hash_
+    assert ledger["grand_total"] == 589824
+
+
+def test_engine_golden_desk_default_and_c1(cuda):
+    z, cond = lp.synthetic_latent((4, 12, 16, 16), 4, 42)
+    out, ledger = lp.run_lp("box", (1, 1, 1), z, 60, 0.05, 3.0, cond, (2, 2, 2), 4, 0.5)
+    assert H(out.to_numpy()) == "18f78847365f6597" and ledger["grand_total"] == 7700480
+    z, cond = lp.synthetic_latent((16, 5, 16, 16), 4, 2025)
+    out, ledger = lp.run_lp("box", (1, 1, 1), z, 4, 0.05, 5.0, cond, (1, 2, 2), 2, 0.5)
+    assert H(out.to_numpy()) == "93a6824b0e691fdc" and ledger["grand_total"] == 442368
+
+
+def test_engine_matches_oracle_sweep(cuda, oracle):
+    for shape, patch, k, r, step, d, seed in _cases(4, 16):
+        try:
+            for s in (1, 2, 3):
+                lp.build_plan(shape, patch, s, k, r)
+        except lp.LpError:
+            continue
+        z, cond = oracle.synthetic(shape, d, seed)
+        for kind, name in [(0, "box"), (1, "global"), (2, "identity")]:
+            radius = (1, 0, 2)
+            want, lw = oracle.run_lp(kind, radius, z, d, 4, 0.05, 3.0, cond, patch, k, r)
+            got, lg = lp.run_lp(name, radius, lp.LatentTensor.from_numpy(z, d), 4, 0.05, 3.0, list(cond), patch, k, r)
+            assert np.array_equal(got.to_numpy(), want) and lg["grand_total"] == lw, (name, shape, patch, k, r, d)
+
+
+def test_single_worker_equals_centralized(cuda, reference):
+    z, cond = lp.synthetic_latent((1, 8, 8, 8), 4, 11)
+    central = reference.run_centralized(0, (1, 1, 1), z.to_numpy(), 4, 3, 0.1, 2.0, cond)
+    final, ledger = lp.run_lp("box", (1, 1, 1), z, 3, 0.1, 2.0, cond, (2, 2, 2), 1, 0.0)
+    assert ledger["grand_total"] == 0
+    assert np.array_equal(final.to_numpy(), central)
+
+
+def test_c2_full_size_engine_vs_oracle(cuda, oracle):
+    # BASELINE config C2 shape (16x21x60x104, f32, seed 2025, K=4, r=0.5) through one
+    # full T->H->W rotation with the box denoiser: bit-exact at full size.
+    dims = (16, 21, 60, 104)
+    z, cond = oracle.synthetic(dims, 4, 2025)
+    want, lw = oracle.run_lp(0, (1, 1, 1), z, 4, 3, 0.05, 5.0, cond, (1, 2, 2), 4, 0.5)
+    got, lg = lp.run_lp("box", (1, 1, 1), lp.LatentTensor.from_numpy(z, 4), 3, 0.05, 5.0, list(cond), (1, 2, 2), 4, 0.5)
+    assert lg["grand_total"] == lw
+    assert np.array_equal(got.to_numpy(), want)
+
+
+def test_nonfinite_is_reported(cuda):
+    z = lp.LatentTensor.from_numpy(np.full((1, 2, 2, 2), 60000.0), 2)
+    lp.device_flags(reset=True)
+    lp.cfg_predict(lp.IdentityDenoiser(), z, 1, [1.0] * 8, 3.0)  # f16 saturates, stays finite
+    assert lp.device_flags() == 0

@@ -1,0 +1,328 @@
+// dit_kernels.cu — the DiT's non-GEMM kernels (memory-bound, fused):
+//   patch gather (K2 prologue: sub-latent -> [tokens, 64] bf16 patches)
+//   time embedding (sinusoid -> MLP -> 6-way modulation), GEMV on CUDA cores
+//   LayerNorm + adaLN modulate -> bf16 (K4), affine LayerNorm -> bf16
+//   q/k RMSNorm + 3-D RoPE in place on the QKV buffer
+//   head unpatchify + CFG combine + quantize to the storage dtype (K8)
+//   pinned weight / text-context generator
+#include <cuda_bf16.h>
+
+#include "dit_kernels.hpp"
+
+namespace lpb200 {
+
+// ---------------------------------------------------------------------------
+// pinned generator: splitmix64(seed, stream, index) -> uniform [-1, 1)
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__host__ __device__ __forceinline__ float hash_uniform(uint64_t seed, uint64_t stream, uint64_t i) {
+    const uint64_t h = splitmix64(splitmix64(seed ^ (stream * 0xD1B54A32D192ED03ull)) + i);
+    return static_cast<float>(static_cast<double>(h >> 40) * (1.0 / 8388608.0) - 1.0);  // 24-bit, [-1, 1)
+}
+
+__global__ void k_init_param(void* p, int64_t n, int is_bf16, uint64_t seed, uint64_t stream, float scale,
+                             float offset) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = offset + scale * hash_uniform(seed, stream, static_cast<uint64_t>(i));
+        if (is_bf16) static_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v);
+        else static_cast<float*>(p)[i] = v;
+    }
+}
+
+void init_param(void* p, int64_t n, bool bf16, uint64_t seed, uint64_t stream, float scale, float offset,
+                cudaStream_t st) {
+    k_init_param<<<592, 256, 0, st>>>(p, n, bf16 ? 1 : 0, seed, stream, scale, offset);
+    LP_LAUNCH_CHECK();
+}
+
+// synthetic text context: N(0,1) via Box-Muller on two hash uniforms -> bf16
+__global__ void k_text_context(__nv_bfloat16* out, int64_t n, uint64_t seed) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float u1 = 0.5f * (hash_uniform(seed, 0x7e47, 2 * i) + 1.f);
+        const float u2 = 0.5f * (hash_uniform(seed, 0x7e47, 2 * i + 1) + 1.f);
+        const float r = sqrtf(-2.f * logf(fmaxf(u1, 1e-7f)));
+        out[i] = __float2bfloat16_rn(r * cosf(6.283185307179586f * u2));
+    }
+}
+void text_context(__nv_bfloat16* out, int64_t n, uint64_t seed, cudaStream_t st) {
+    k_text_context<<<592, 256, 0, st>>>(out, n, seed);
+    LP_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// patch gather: sub-latent [C, F, H, W] (storage dtype) -> patches [tok, C*pt*ph*pw]
+// bf16, token = (f, y, x) row-major, feature = ((c*pt + kt)*ph + kh)*pw + kw
+// (Conv3d weight flattening); positions past the extent are zero (padding).
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void k_patchify(const typename Store<D>::T* __restrict__ z, __nv_bfloat16* __restrict__ out, int C, int F,
+                           int H, int W, int pt, int ph, int pw, int nf, int nh, int nw) {
+    const int feat = C * pt * ph * pw;
+    const int64_t total = static_cast<int64_t>(nf) * nh * nw * feat;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int fe = static_cast<int>(i % feat);
+        const int64_t tok = i / feat;
+        const int xw = static_cast<int>(tok % nw), yh = static_cast<int>((tok / nw) % nh), tf = static_cast<int>(tok / (static_cast<int64_t>(nw) * nh));
+        const int kw = fe % pw, kh = (fe / pw) % ph, kt = (fe / (pw * ph)) % pt, c = fe / (pw * ph * pt);
+        const int t = tf * pt + kt, y = yh * ph + kh, x = xw * pw + kw;
+        float v = 0.f;
+        if (t < F && y < H && x < W) v = static_cast<float>(load_val<D>(z, ((static_cast<int64_t>(c) * F + t) * H + y) * W + x));
+        out[i] = __float2bfloat16_rn(v);
+    }
+}
+
+void patchify(const void* z, int dtype, const int shape[4], const int patch[3], __nv_bfloat16* out, cudaStream_t st) {
+    const int nf = (shape[1] + patch[0] - 1) / patch[0], nh = (shape[2] + patch[1] - 1) / patch[1],
+              nw = (shape[3] + patch[2] - 1) / patch[2];
+    const int64_t total = static_cast<int64_t>(nf) * nh * nw * shape[0] * patch[0] * patch[1] * patch[2];
+    const int g = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+#define LP_PATCH(DD) k_patchify<DD><<<g, 256, 0, st>>>(static_cast<const typename Store<DD>::T*>(z), out, shape[0], shape[1], shape[2], shape[3], patch[0], patch[1], patch[2], nf, nh, nw)
+    if (dtype == 2) LP_PATCH(2);
+    else if (dtype == 4) LP_PATCH(4);
+    else LP_PATCH(8);
+#undef LP_PATCH
+    LP_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// GEMV for the time path: y[o] = act_out( W[o,:] · act_in(x) + b[o] ) (+ add[o])
+// W bf16 row-major [out, in]; one warp per output.  act: 0 none, 1 SiLU
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float silu(float x) { return x / (1.f + __expf(-x)); }
+
+__global__ void k_gemv(const __nv_bfloat16* __restrict__ W, const float* __restrict__ bias,
+                       const float* __restrict__ x, float* __restrict__ y, int in, int out, int act_in) {
+    const int o = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (o >= out) return;
+    float acc = 0.f;
+    for (int i = lane; i < in; i += 32) {
+        float v = x[i];
+        if (act_in) v = silu(v);
+        acc += __bfloat162float(W[static_cast<int64_t>(o) * in + i]) * v;
+    }
+#pragma unroll
+    for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, s);
+    if (lane == 0) y[o] = acc + (bias ? bias[o] : 0.f);
+}
+
+// sinusoid embedding: [cos(t*w_i), sin(t*w_i)], w_i = 10000^(-i/half)
+__global__ void k_sinusoid(float* out, int dim, float t) {
+    const int half = dim / 2;
+    for (int i = threadIdx.x; i < half; i += blockDim.x) {
+        const double w = pow(10000.0, -static_cast<double>(i) / half);
+        const double a = static_cast<double>(t) * w;
+        out[i] = static_cast<float>(cos(a));
+        out[i + half] = static_cast<float>(sin(a));
+    }
+}
+
+// mod[l, j, :] = param[l, j, :] + e0[j, :]   (j < 6), head: hmod[j] = hparam[j] + e[:]
+__global__ void k_add_mod(const float* __restrict__ param, const float* __restrict__ e0, float* __restrict__ out,
+                          int64_t per_layer, int64_t layers) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per_layer * layers;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = param[i] + e0[i % per_layer];
+}
+
+void time_embedding(const TimeWeights& w, float t, int freq_dim, int dim, int layers, float* scratch,
+                    float* mod_out, float* head_mod_out, cudaStream_t st) {
+    float* sin_ = scratch;                 // [freq_dim]
+    float* h1 = sin_ + freq_dim;           // [dim]
+    float* e = h1 + dim;                   // [dim]
+    float* e0 = e + dim;                   // [6*dim]
+    k_sinusoid<<<1, 256, 0, st>>>(sin_, freq_dim, t);
+    LP_LAUNCH_CHECK();
+    k_gemv<<<(dim + 7) / 8, 256, 0, st>>>(w.w1, w.b1, sin_, h1, freq_dim, dim, 0);
+    LP_LAUNCH_CHECK();
+    k_gemv<<<(dim + 7) / 8, 256, 0, st>>>(w.w2, w.b2, h1, e, dim, dim, 1);
+    LP_LAUNCH_CHECK();
+    k_gemv<<<(6 * dim + 7) / 8, 256, 0, st>>>(w.wp, w.bp, e, e0, dim, 6 * dim, 1);
+    LP_LAUNCH_CHECK();
+    k_add_mod<<<296, 256, 0, st>>>(w.block_mod, e0, mod_out, 6LL * dim, layers);
+    LP_LAUNCH_CHECK();
+    k_add_mod<<<8, 256, 0, st>>>(w.head_mod, e, head_mod_out, dim, 2);
+    LP_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// LayerNorm (+ modulate | + affine) fp32 -> bf16, one warp per row, d % 256 == 0
+//   MOD:    y = LN(x) * (1 + scale) + shift
+//   AFFINE: y = LN(x) * weight + bias
+// ---------------------------------------------------------------------------
+template <int PER, bool AFFINE>
+__global__ void __launch_bounds__(256) k_layernorm(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                                                   int64_t rows, int d, const float* __restrict__ a,
+                                                   const float* __restrict__ b, float eps) {
+    const int64_t row = blockIdx.x * 8LL + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const float4* xr = reinterpret_cast<const float4*>(x + row * d);
+    float v[PER * 4];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const float4 q = xr[lane + 32 * i];
+        v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
+        s += q.x + q.y + q.z + q.w;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+    const float mean = s / d;
+    float var = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER * 4; ++i) {
+        const float c = v[i] - mean;
+        var += c * c;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffff, var, o);
+    const float rstd = rsqrtf(var / d + eps);
+    uint2* yr = reinterpret_cast<uint2*>(y + row * d);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int c0 = 4 * (lane + 32 * i);
+        float o4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float n = (v[4 * i + u] - mean) * rstd;
+            o4[u] = AFFINE ? n * a[c0 + u] + b[c0 + u] : n * (1.f + a[c0 + u]) + b[c0 + u];
+        }
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(o4[0], o4[1]), p1 = __floats2bfloat162_rn(o4[2], o4[3]);
+        yr[lane + 32 * i] = make_uint2(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1));
+    }
+}
+
+void layernorm_bf16(const float* x, __nv_bfloat16* y, int64_t rows, int d, const float* a, const float* b, bool affine,
+                    float eps, cudaStream_t st) {
+    if (d % 128) fail(LP_ERR_INVALID_ARGUMENT, "layernorm: d must be a multiple of 128");
+    const int per = d / 128;
+    const unsigned g = static_cast<unsigned>((rows + 7) / 8);
+#define LP_LN(P)                                                                                 \
+    if (per == P) {                                                                              \
+        if (affine) k_layernorm<P, true><<<g, 256, 0, st>>>(x, y, rows, d, a, b, eps);           \
+        else k_layernorm<P, false><<<g, 256, 0, st>>>(x, y, rows, d, a, b, eps);                 \
+        LP_LAUNCH_CHECK();                                                                       \
+        return;                                                                                  \
+    }
+    LP_LN(1) LP_LN(2) LP_LN(4) LP_LN(8) LP_LN(12) LP_LN(16) LP_LN(24) LP_LN(32) LP_LN(40)
+#undef LP_LN
+    fail(LP_ERR_INVALID_ARGUMENT, "layernorm: unsupported width");
+}
+
+// ---------------------------------------------------------------------------
+// RMSNorm over the full width d of a [rows, ld] bf16 slice (cols [col0, col0+d)),
+// times weight g, then (optionally) 3-D RoPE per 128-wide head, in place.
+// RoPE (WAN2.1): head_dim 128 = 64 complex pairs; pairs [0,22) rotate with the
+// frame index, [22,43) with the row, [43,64) with the column; pair j of a part
+// with P pairs uses theta^(-j/P) (theta 10000), i.e. rope_params(1024, 2P).
+// ---------------------------------------------------------------------------
+template <int PER>
+__global__ void __launch_bounds__(256) k_rmsnorm_rope(__nv_bfloat16* __restrict__ buf, int64_t rows, int64_t ld,
+                                                      int64_t col0, int d, const float* __restrict__ g, float eps,
+                                                      int rope, int64_t rows_per_batch, int nh, int nw) {
+    const int64_t row = blockIdx.x * 8LL + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    __nv_bfloat16* p = buf + row * ld + col0;
+    // lane owns pairs: element index e = 2*(lane + 32*i) for i < PER (d = 64*PER)
+    float v[2 * PER];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const __nv_bfloat162 q = reinterpret_cast<const __nv_bfloat162*>(p)[lane + 32 * i];
+        v[2 * i] = __bfloat162float(q.x);
+        v[2 * i + 1] = __bfloat162float(q.y);
+        ss += v[2 * i] * v[2 * i] + v[2 * i + 1] * v[2 * i + 1];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+    const float r = rsqrtf(ss / d + eps);
+    int pf = 0, py = 0, px = 0;
+    if (rope) {
+        const int64_t tok = row % rows_per_batch;
+        px = static_cast<int>(tok % nw);
+        py = static_cast<int>((tok / nw) % nh);
+        pf = static_cast<int>(tok / (static_cast<int64_t>(nw) * nh));
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int e = 2 * (lane + 32 * i);
+        float a = v[2 * i] * r * g[e], b = v[2 * i + 1] * r * g[e + 1];
+        if (rope) {
+            const int j = (e & 127) >> 1;  // pair within the head
+            int pos, jj, P;
+            if (j < 22) { pos = pf; jj = j; P = 22; }
+            else if (j < 43) { pos = py; jj = j - 22; P = 21; }
+            else { pos = px; jj = j - 43; P = 21; }
+            const float freq = exp2f(-13.287712379549449f * static_cast<float>(jj) / static_cast<float>(P));  // 10000^(-jj/P)
+            float sn, cs;
+            sincosf(static_cast<float>(pos) * freq, &sn, &cs);
+            const float a2 = a * cs - b * sn, b2 = a * sn + b * cs;
+            a = a2;
+            b = b2;
+        }
+        reinterpret_cast<__nv_bfloat162*>(p)[lane + 32 * i] = __floats2bfloat162_rn(a, b);
+    }
+}
+
+void rmsnorm_rope(__nv_bfloat16* buf, int64_t rows, int64_t ld, int64_t col0, int d, const float* g, float eps,
+                  bool rope, int64_t rows_per_batch, int nh, int nw, cudaStream_t st) {
+    if (d % 64) fail(LP_ERR_INVALID_ARGUMENT, "rmsnorm: d must be a multiple of 64");
+    const int per = d / 64;
+    const unsigned gr = static_cast<unsigned>((rows + 7) / 8);
+#define LP_RMS(P)                                                                                               \
+    if (per == P) {                                                                                             \
+        k_rmsnorm_rope<P><<<gr, 256, 0, st>>>(buf, rows, ld, col0, d, g, eps, rope ? 1 : 0, rows_per_batch, nh, nw); \
+        LP_LAUNCH_CHECK();                                                                                      \
+        return;                                                                                                 \
+    }
+    LP_RMS(1) LP_RMS(2) LP_RMS(4) LP_RMS(8) LP_RMS(16) LP_RMS(24) LP_RMS(32) LP_RMS(48) LP_RMS(64) LP_RMS(80)
+#undef LP_RMS
+    fail(LP_ERR_INVALID_ARGUMENT, "rmsnorm: unsupported width");
+}
+
+// ---------------------------------------------------------------------------
+// head output [2*ntok, C*pt*ph*pw] fp32 (feature = ((kt*ph + kh)*pw + kw)*C + c)
+// -> unpatchify, crop, CFG: eps = q(u + w (c - u)) with u, c quantized first
+// (cfg_predict, src/denoise.cpp:24-39), fp64 combine, stored in the storage dtype.
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void k_unpatchify_cfg(const float* __restrict__ head, typename Store<D>::T* __restrict__ eps, int C, int F,
+                                 int H, int W, int pt, int ph, int pw, int nh, int nw, int64_t ntok, double w) {
+    const int64_t total = static_cast<int64_t>(C) * F * H * W;
+    const int feat = C * pt * ph * pw;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int x = static_cast<int>(i % W);
+        const int y = static_cast<int>((i / W) % H);
+        const int t = static_cast<int>((i / (static_cast<int64_t>(W) * H)) % F);
+        const int c = static_cast<int>(i / (static_cast<int64_t>(W) * H * F));
+        const int64_t tok = (static_cast<int64_t>(t / pt) * nh + y / ph) * nw + x / pw;
+        const int fe = (((t % pt) * ph + (y % ph)) * pw + (x % pw)) * C + c;
+        const double u = quantize_dev<D>(static_cast<double>(head[tok * feat + fe]));
+        const double cc = quantize_dev<D>(static_cast<double>(head[(ntok + tok) * feat + fe]));
+        store_q<D>(eps, i, __dadd_rn(u, __dmul_rn(w, __dsub_rn(cc, u))));
+    }
+}
+
+void unpatchify_cfg(const float* head, int dtype, const int shape[4], const int patch[3], double w, void* eps,
+                    cudaStream_t st) {
+    const int nh = (shape[2] + patch[1] - 1) / patch[1], nw = (shape[3] + patch[2] - 1) / patch[2];
+    const int nf = (shape[1] + patch[0] - 1) / patch[0];
+    const int64_t ntok = static_cast<int64_t>(nf) * nh * nw;
+    const int64_t total = static_cast<int64_t>(shape[0]) * shape[1] * shape[2] * shape[3];
+    const int g = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+#define LP_UNP(DD) k_unpatchify_cfg<DD><<<g, 256, 0, st>>>(head, static_cast<typename Store<DD>::T*>(eps), shape[0], shape[1], shape[2], shape[3], patch[0], patch[1], patch[2], nh, nw, ntok, w)
+    if (dtype == 2) LP_UNP(2);
+    else if (dtype == 4) LP_UNP(4);
+    else LP_UNP(8);
+#undef LP_UNP
+    LP_LAUNCH_CHECK();
+}
+
+}  // namespace lpb200

@@ -1,0 +1,34 @@
+// dit_kernels.hpp — launchers of the DiT's memory-bound kernels (dit_kernels.cu).
+#pragma once
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace lpb200 {
+
+struct TimeWeights {
+    const __nv_bfloat16* w1; const float* b1;  // [dim, freq_dim]
+    const __nv_bfloat16* w2; const float* b2;  // [dim, dim]
+    const __nv_bfloat16* wp; const float* bp;  // [6*dim, dim]
+    const float* block_mod;                     // [layers, 6, dim]
+    const float* head_mod;                      // [2, dim]
+};
+
+void init_param(void* p, int64_t n, bool bf16, uint64_t seed, uint64_t stream, float scale, float offset,
+                cudaStream_t st);
+void text_context(__nv_bfloat16* out, int64_t n, uint64_t seed, cudaStream_t st);
+void patchify(const void* z, int dtype, const int shape[4], const int patch[3], __nv_bfloat16* out, cudaStream_t st);
+// scratch >= freq_dim + 8*dim floats; mod_out [layers, 6, dim]; head_mod_out [2, dim]
+void time_embedding(const TimeWeights& w, float t, int freq_dim, int dim, int layers, float* scratch, float* mod_out,
+                    float* head_mod_out, cudaStream_t st);
+void layernorm_bf16(const float* x, __nv_bfloat16* y, int64_t rows, int d, const float* a, const float* b, bool affine,
+                    float eps, cudaStream_t st);
+void rmsnorm_rope(__nv_bfloat16* buf, int64_t rows, int64_t ld, int64_t col0, int d, const float* g, float eps,
+                  bool rope, int64_t rows_per_batch, int nh, int nw, cudaStream_t st);
+void unpatchify_cfg(const float* head, int dtype, const int shape[4], const int patch[3], double w, void* eps,
+                    cudaStream_t st);
+
+}  // namespace lpb200

@@ -1,0 +1,310 @@
+// gemm_tcgen05.cu — persistent, warp-specialized tcgen05 GEMM for sm_100a.
+//
+//   D[M,N] = epilogue( A[M,K] · B[N,K]^T )      A, B bf16, K-major (row-major, K contiguous)
+//
+// Roles (192 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one lane),
+// warps 2..5 = epilogue (TMEM -> registers -> global), warp 2 also owns TMEM.
+// Tiles 128 x BN x 64 (BN = 256/128/64), 4-stage smem ring fed by TMA with
+// 128-byte swizzle, accumulators double-buffered in TMEM (2 x BN columns) so
+// the epilogue of tile i overlaps the MMAs of tile i+1.  Raster: consecutive
+// tiles walk N first, so the 148 co-resident CTAs share A rows through L2 and
+// the whole weight matrix stays L2-resident.
+//
+// Epilogues fused into the DiT's dense layers:
+//   BF16       out_bf16 = acc + bias
+//   BF16_GELU  out_bf16 = gelu_tanh(acc + bias)          (FFN1)
+//   F32_RESID  x_f32   += (acc + bias) * gate[col]       (attn-O / FFN2 gated residual)
+//   F32        out_f32  = acc + bias                      (head)
+#include <cuda.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "dit_ops.hpp"
+#include "tc_ptx.cuh"
+
+namespace lpb200 {
+
+using namespace tc;
+
+// ---------------------------------------------------------------------------
+// TMA descriptors (host)
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    if (!fn) fail(LP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+CUtensorMap make_tmap_2d_bf16(const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
+                              uint32_t box_inner, uint32_t box_outer, bool swizzle128) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {inner, outer};
+    const cuuint64_t strides[1] = {row_stride_bytes};
+    const cuuint32_t box[2] = {box_inner, box_outer};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(LP_ERR_CUDA, "cuTensorMapEncodeTiled(2d) failed: " + std::to_string(r));
+    return m;
+}
+
+CUtensorMap make_tmap_3d_bf16(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
+                              uint32_t b0, uint32_t b1, uint32_t b2) {
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {d0, d1, d2};
+    const cuuint64_t strides[2] = {s1, s2};
+    const cuuint32_t box[3] = {b0, b1, b2};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(LP_ERR_CUDA, "cuTensorMapEncodeTiled(3d) failed: " + std::to_string(r));
+    return m;
+}
+
+// ---------------------------------------------------------------------------
+// Kernel
+// ---------------------------------------------------------------------------
+constexpr int kBM = 128, kBK = 64, kStages = 4, kGemmThreads = 192;
+
+template <int BN>
+constexpr int gemm_smem_bytes() {
+    return kStages * (kBM * kBK * 2 + BN * kBK * 2) + 1024 /*align*/ + 256 /*barriers*/;
+}
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+    const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+    return 0.5f * x * (1.f + t);
+}
+
+template <int BN, int MODE>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, GemmEpilogue ep, int M,
+           int N, int K) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int A_BYTES = kBM * kBK * 2, B_BYTES = BN * kBK * 2;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kStages * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * B_BYTES);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const int num_n = N / BN, num_m = (M + kBM - 1) / kBM, tiles = num_m * num_n;
+    const int nk = (K + kBK - 1) / kBK;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tma);
+        tma_prefetch(&tmb);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512))));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int mb = t / num_n, nb = t % num_n;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
+                    tma_load_2d(&tma, &full[s], sA + s * A_BYTES, kb * kBK, mb * kBM);
+                    tma_load_2d(&tmb, &full[s], sB + s * B_BYTES, kb * kBK, nb * BN);
+                    if (++s == kStages) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16(kBM, BN);
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+                const int acc = it & 1;
+                const uint32_t aph = (it >> 1) & 1;
+                mbar_wait(&tempty[acc], aph ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k)
+                        mma_ss(d, desc_sw128(a0 + k * 32), desc_sw128(b0 + k * 32), idesc, (kb | k) != 0);
+                    mma_commit(&empty[s]);
+                    if (++s == kStages) { s = 0; ph ^= 1; }
+                }
+                mma_commit(&tfull[acc]);
+            }
+        }
+    } else {
+        // epilogue: warps 2..5 -> TMEM lane quadrant warp % 4
+        const uint32_t q = warp & 3;
+        int it = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+            const int mb = t / num_n, nb = t % num_n;
+            const int acc = it & 1;
+            const uint32_t aph = (it >> 1) & 1;
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            const int row = mb * kBM + q * 32 + lane;
+            const uint32_t taddr = tmem + ((q * 32) << 16) + acc * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t r[32];
+                tmem_ld32(taddr + c, r);
+                tmem_ld_wait();
+                if (row < M) {
+                    const int col0 = nb * BN + c;
+                    float v[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + (ep.bias ? __ldg(ep.bias + col0 + j) : 0.f);
+                    if (MODE == EPI_BF16 || MODE == EPI_BF16_GELU) {
+                        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + col0;
+                        uint4* o4 = reinterpret_cast<uint4*>(o);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            float a[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) a[u] = MODE == EPI_BF16_GELU ? gelu_tanh(v[8 * j + u]) : v[8 * j + u];
+                            o4[j] = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]),
+                                               pack_bf16(a[6], a[7]));
+                        }
+                    } else {
+                        float* o = static_cast<float*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + col0;
+                        float4* o4 = reinterpret_cast<float4*>(o);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            float4 x;
+                            if (MODE == EPI_F32_RESID) {
+                                x = o4[j];
+                                const float* g = ep.gate ? ep.gate + col0 + 4 * j : nullptr;
+                                x.x += v[4 * j + 0] * (g ? __ldg(g + 0) : 1.f);
+                                x.y += v[4 * j + 1] * (g ? __ldg(g + 1) : 1.f);
+                                x.z += v[4 * j + 2] * (g ? __ldg(g + 2) : 1.f);
+                                x.w += v[4 * j + 3] * (g ? __ldg(g + 3) : 1.f);
+                            } else {
+                                x = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                            }
+                            o4[j] = x;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 2) tmem_dealloc(tmem, 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512))));
+}
+
+// ---------------------------------------------------------------------------
+// Host launch
+// ---------------------------------------------------------------------------
+static int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
+template <int BN, int MODE>
+static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmEpilogue& ep, int M, int N, int K,
+                        cudaStream_t st) {
+    constexpr int smem = gemm_smem_bytes<BN>();
+    static bool attr = false;
+    if (!attr) {
+        LP_CUDA(cudaFuncSetAttribute(k_gemm<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    const int tiles = ((M + kBM - 1) / kBM) * (N / BN);
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    k_gemm<BN, MODE><<<grid, kGemmThreads, smem, st>>>(ta, tb, ep, M, N, K);
+    LP_LAUNCH_CHECK();
+}
+
+template <int MODE>
+static void gemm_bn(const CUtensorMap& ta, const void* B, int64_t ldb, const GemmEpilogue& ep, int M, int N, int K,
+                    cudaStream_t st) {
+    if (N % 256 == 0) {
+        const CUtensorMap tb = make_tmap_2d_bf16(B, K, N, ldb * 2, kBK, 256);
+        launch_gemm<256, MODE>(ta, tb, ep, M, N, K, st);
+    } else if (N % 128 == 0) {
+        const CUtensorMap tb = make_tmap_2d_bf16(B, K, N, ldb * 2, kBK, 128);
+        launch_gemm<128, MODE>(ta, tb, ep, M, N, K, st);
+    } else if (N % 64 == 0) {
+        const CUtensorMap tb = make_tmap_2d_bf16(B, K, N, ldb * 2, kBK, 64);
+        launch_gemm<64, MODE>(ta, tb, ep, M, N, K, st);
+    } else {
+        fail(LP_ERR_INVALID_ARGUMENT, "gemm: N must be a multiple of 64");
+    }
+}
+
+void gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const GemmEpilogue& ep,
+               int mode, cudaStream_t st) {
+    if (M <= 0) return;
+    if (K % 8 || lda % 8 || ldb % 8) fail(LP_ERR_INVALID_ARGUMENT, "gemm: K and strides must be multiples of 8");
+    const CUtensorMap ta = make_tmap_2d_bf16(A, K, M, lda * 2, kBK, kBM);
+    switch (mode) {
+        case EPI_BF16: gemm_bn<EPI_BF16>(ta, B, ldb, ep, M, N, K, st); break;
+        case EPI_BF16_GELU: gemm_bn<EPI_BF16_GELU>(ta, B, ldb, ep, M, N, K, st); break;
+        case EPI_F32_RESID: gemm_bn<EPI_F32_RESID>(ta, B, ldb, ep, M, N, K, st); break;
+        case EPI_F32: gemm_bn<EPI_F32>(ta, B, ldb, ep, M, N, K, st); break;
+        default: fail(LP_ERR_INVALID_ARGUMENT, "gemm: bad epilogue");
+    }
+}
+
+}  // namespace lpb200
+
+using namespace lpb200;
+
+extern "C" int lp_gemm_bf16(const void* A, const void* B, const void* bias, void* D, int64_t M, int64_t N, int64_t K,
+                            void* stream) {
+    return guard([&] {
+        GemmEpilogue ep{};
+        ep.bias = static_cast<const float*>(bias);
+        ep.out = D;
+        ep.ldo = N;
+        gemm_bf16(A, K, B, K, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), ep, EPI_BF16,
+                  as_stream(stream));
+    });
+}

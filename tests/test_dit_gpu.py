@@ -1,0 +1,132 @@
+"""GPU numerics of the DiT kernels against plain PyTorch fp32 references.
+
+Tolerances (bf16 operands, fp32 accumulation):
+  GEMM       |D - ref| <= 2e-2 * max|ref| + 1e-2   (bf16 output rounding + K-long sums)
+  attention  |O - ref| <= 2e-2                     (P in bf16, |O| <= max|V| ~ 3)
+  DiT eps    rel. L2 error <= 5e-2 after 2 blocks  (bf16 activations through 2 blocks)
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2512_07350_b200 import _lib, lp
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm(A, B, bias):
+    M, K = A.shape
+    N = B.shape[0]
+    D = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    _lib.check(_lib.lib().lp_gemm_bf16(C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()),
+                                       C.c_void_p(bias.data_ptr()) if bias is not None else None,
+                                       C.c_void_p(D.data_ptr()), M, N, K,
+                                       C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return D
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 256, 128), (300, 1536, 1536), (130, 128, 4096),
+                                   (1000, 64, 1536), (65, 4608, 1536), (4096, 8960, 1536), (2000, 1536, 8960)])
+def test_gemm_matches_torch(cuda, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g)
+    D = _gemm(A, B, bias).float()
+    ref = A.float() @ B.float().t() + bias
+    err = (D - ref).abs().max().item()
+    assert err <= 2e-2 * ref.abs().max().item() + 1e-2, err
+
+
+def _attn(q, k, v, scale):
+    B, S, H, _ = q.shape
+    Skv = k.shape[1]
+    o = torch.empty_like(q)
+    _lib.check(_lib.lib().lp_attention_bf16(C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()),
+                                            C.c_void_p(v.data_ptr()), C.c_void_p(o.data_ptr()), B, S, Skv, H, scale,
+                                            C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return o
+
+
+@pytest.mark.parametrize("B,S,Skv,H", [(1, 128, 128, 1), (2, 200, 200, 3), (2, 300, 512, 2), (1, 1024, 1024, 2),
+                                       (2, 1560, 1560, 12), (1, 129, 1000, 1)])
+def test_attention_matches_torch(cuda, B, S, Skv, H):
+    g = torch.Generator(device="cuda").manual_seed(S * 31 + Skv + H)
+    q = torch.randn(B, S, H, 128, device="cuda", generator=g).bfloat16()
+    k = torch.randn(B, Skv, H, 128, device="cuda", generator=g).bfloat16()
+    v = torch.randn(B, Skv, H, 128, device="cuda", generator=g).bfloat16()
+    scale = 1.0 / 128 ** 0.5
+    o = _attn(q, k, v, scale).float()
+    ref = torch.nn.functional.scaled_dot_product_attention(q.float().transpose(1, 2), k.float().transpose(1, 2),
+                                                           v.float().transpose(1, 2)).transpose(1, 2)
+    err = (o - ref).abs().max().item()
+    assert err <= 2e-2, err
+
+
+def test_attention_large_logits(cuda):
+    # scores far from 0 exercise the lazy-rescale path (max jumps by > 8 in log2 units)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q = (torch.randn(1, 512, 1, 128, device="cuda", generator=g) * 4).bfloat16()
+    k = (torch.randn(1, 512, 1, 128, device="cuda", generator=g) * 4).bfloat16()
+    v = torch.randn(1, 512, 1, 128, device="cuda", generator=g).bfloat16()
+    o = _attn(q, k, v, 1 / 128 ** 0.5).float()
+    ref = torch.nn.functional.scaled_dot_product_attention(q.float().transpose(1, 2), k.float().transpose(1, 2),
+                                                           v.float().transpose(1, 2)).transpose(1, 2)
+    assert (o - ref).abs().max().item() <= 3e-2
+
+
+def _dit_case(layers=2, shape=(16, 5, 16, 16), t=37, w=5.0):
+    from tests.dit_reference import DiTReference
+
+    z, cond = lp.synthetic_latent(shape, 4, 2025)
+    dit = lp.DiTDenoiser(cond, num_layers=layers)
+    eps = dit.cfg_predict(z, t, w)
+    torch.cuda.synchronize()
+    ref = DiTReference(dit)
+    L = dit.cfg.num_layers
+    ck = [dit.debug_tensor(f"ctx_k.{l}", torch.bfloat16).float().view(2, dit.cfg.text_len, -1) for l in range(L)]
+    cv = [dit.debug_tensor(f"ctx_v.{l}", torch.bfloat16).float().view(2, dit.cfg.text_len, -1) for l in range(L)]
+    want, head_ref = ref.forward(z.data.float(), t, ck, cv, w)
+    head = dit.debug_tensor("head", torch.float32).view(head_ref.shape)
+    return eps, want, head, head_ref, dit
+
+
+def test_dit_forward_matches_torch_fp32(cuda):
+    eps, want, head, head_ref, _ = _dit_case()
+    rel_head = ((head - head_ref).norm() / head_ref.norm()).item()
+    rel = ((eps.data.float() - want).norm() / want.norm()).item()
+    assert np.isfinite(rel) and rel <= 5e-2, (rel, rel_head)
+    assert rel_head <= 5e-2
+
+
+def test_dit_forward_odd_shard_shape(cuda):
+    # remainder rows (W=19, H=9 not multiples of the patch) are zero-padded and cropped
+    eps, want, _, _, _ = _dit_case(layers=1, shape=(16, 3, 9, 19), t=3, w=2.0)
+    rel = ((eps.data.float() - want).norm() / want.norm()).item()
+    assert rel <= 5e-2, rel
+
+
+def test_dit_text_context_matches_reference_mlp(cuda):
+    _, _, _, _, dit = _dit_case(layers=1)
+    from tests.dit_reference import DiTReference, rms
+
+    ref = DiTReference(dit)
+    k0 = dit.debug_tensor("ctx_k.0", torch.bfloat16).float().view(2, dit.cfg.text_len, -1)
+    # uncond context rows are the null (zero) text: MLP of zeros, then K projection + RMSNorm
+    ctx0 = ref.context(torch.zeros(1, dit.cfg.text_len, dit.cfg.text_dim, device="cuda"))[0]
+    k_ref = rms(ctx0 @ ref.p["blocks.0.ck.w"].view(dit.cfg.dim, -1).t() + ref.p["blocks.0.ck.b"],
+                ref.p["blocks.0.cnorm_k"], dit.cfg.eps)
+    assert ((k0[0] - k_ref).norm() / k_ref.norm()).item() <= 2e-2
+
+
+def test_engine_dit_step_runs(cuda):
+    z, cond = lp.synthetic_latent((16, 5, 16, 16), 4, 2025)
+    dit = lp.DiTDenoiser(cond, num_layers=2)
+    eng = lp.LpEngine((16, 5, 16, 16), (1, 2, 2), 4, 2, 0.5, 3, 0.05, 5.0, cond, denoiser="dit", dit=dit)
+    eng.load(z)
+    eng.run(1, 3)
+    torch.cuda.synchronize()
+    assert torch.isfinite(eng.z.data).all()
+    assert eng.launches() > 0

@@ -1,0 +1,318 @@
+"""LP denoise benchmark (BASELINE.json metric: LP denoise steps/s, WAN-1.3B-shape
+480p 81f; comm bytes/video).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload (BASELINE.json configs[1], "C2"): WAN2.1-1.3B-shaped random-init DiT
+(30 blocks, d=1536, 12 heads, FFN 8960, CFG batch 2) on the 480p/81-frame latent
+16x21x60x104 (f32 storage), patch (1,2,2), LP with K = max(4, N) workers, r = 0.5,
+T = 50-step schedule, eta 0.05, w 5.0, synthetic_inputs seed 2025.  Entries are
+dealt round-robin to the N ranks (N=1 runs all 4 shards on one GPU).  A "step"
+is one LP denoise step: plan, K1 gather, DiT cfg_predict on this rank's shards,
+NCCL all-gather of the eps shards (N>1), K10 blend + sampler update.
+
+`value` is device-timed (CUDA events on the engine stream, max over ranks);
+`e2e` is the same steps through the C-ABI engine with the latent copied in from
+pinned host memory and the result copied back every step.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DIMS = (16, 21, 60, 104)
+PATCH = (1, 2, 2)
+T_SCHED = 50
+ETA, W_CFG, SEED, R_OVERLAP = 0.05, 5.0, 2025, 0.5
+METRIC = "LP denoise steps/s, WAN-1.3B-shape 480p 81f (C2)"
+UNIT = "steps/s"
+
+
+def workload(K, world, layers):
+    return {
+        "workload": f"C2: WAN2.1-1.3B-shaped DiT ({layers} blocks, d=1536, 12 heads, ffn 8960, CFG batch 2) on 480p81f "
+                    f"latent 16x21x60x104 f32, patch (1,2,2), LP K={K} r={R_OVERLAP}, T={T_SCHED}, eta {ETA}, w {W_CFG}",
+        "lp_workers": K, "overlap_ratio": R_OVERLAP, "latent": list(DIMS), "patch": list(PATCH), "schedule_steps": T_SCHED,
+        "ranks": world, "shard_assignment": "round-robin entries over ranks",
+        "l2": "working set > L2 (2.6 GB of bf16 weights streamed per forward, >100 MB activations)",
+    }
+
+
+def step_index(s):
+    return (s - 1) % T_SCHED + 1
+
+
+# ---------------------------------------------------------------------------
+# clocks (NVML) sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, v in self.REASONS.items():
+                    if mask & v and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference's own run_lp (oracle/_ref = unmodified lpsim) at C2
+# ---------------------------------------------------------------------------
+def cpu_reference_run(steps, K, threads):
+    import numpy as np
+
+    from oracle.oracle import Oracle, Reference, reference_available
+
+    os.environ["LPSIM_THREADS"] = str(threads)
+    kind = "reference" if reference_available() else "port"
+    lib = Reference() if kind == "reference" else Oracle()
+    z, cond = lib.synthetic(DIMS, 4, SEED)
+    t0 = time.perf_counter()
+    lib.run_lp(0, (1, 1, 1), z, 4, steps, ETA, W_CFG, cond, PATCH, K, R_OVERLAP)
+    dt = time.perf_counter() - t0
+    used = min(threads, K) if kind == "reference" else 1
+    sample = (f"reference run_lp (box denoiser rho=1 in place of the DiT: the reference has none), C2 latent "
+              f"16x21x60x104 f32, K={K}, r={R_OVERLAP}, {steps} steps; LPSIM_THREADS={threads} "
+              f"(the pool uses min(threads, K) workers; extract/reconstruct/sampler are single-threaded)")
+    del np
+    return steps / dt, {"kind": kind, "cores": used, "sample": sample, "seconds": dt}
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    K = args.workers or max(4, world)
+    threads = os.cpu_count() or 1
+    cpu_reference_run(max(1, args.warmup), K, threads)  # warm-up (untimed)
+    value, info = cpu_reference_run(args.steps, K, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (synthetic_inputs seed 2025)",
+        "config": workload(K, world, 30),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
+                         "sample": info["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_07350_b200 import _lib, lp
+
+    L = _lib.lib()
+    torch.cuda.set_device(local_rank)
+    _lib.check(L.lp_device_check(local_rank))
+    K = args.workers or max(4, world)
+    z_host_np, cond = lp.synthetic_latent_host(DIMS, 4, SEED)
+    dit = lp.DiTDenoiser(cond, num_layers=args.layers)
+    nccl_id = None
+    if world > 1:
+        obj = [lp.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    eng = lp.LpEngine(DIMS, PATCH, 4, K, R_OVERLAP, T_SCHED, ETA, W_CFG, cond, denoiser="dit", dit=dit, world=world,
+                      rank=rank, nccl_id=nccl_id)
+    z0 = torch.from_numpy(z_host_np.astype("float32")).pin_memory()
+    eng.z.data.copy_(z0)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up
+    for s in range(1, args.warmup + 1):
+        eng.run(step_index(s), 1)
+    torch.cuda.synchronize()
+
+    # ---- device-timed region: K steps, inputs resident in HBM ----
+    first = args.warmup + 1
+    c0, l0 = eng.comm(), L.lp_launch_count()
+    L.lp_profile_enable(1)
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for s in range(first, first + args.steps):
+            eng.run(step_index(s), 1)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    L.lp_profile_enable(0)
+    launches = int(L.lp_launch_count() - l0)
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    c1 = eng.comm()
+    nl = (C.c_uint64 * 3)()
+    kms, kfl, kby = (C.c_double * 3)(), (C.c_double * 3)(), (C.c_double * 3)()
+    _lib.check(L.lp_profile_collect(nl, kms, kfl, kby))
+
+    # ---- end-to-end through the C-ABI engine with host buffers ----
+    zin = torch.empty(DIMS, dtype=torch.float32).pin_memory()
+    zin.copy_(z0)
+    zout = torch.empty_like(zin).pin_memory()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for s in range(first, first + args.steps):
+        eng.z.data.copy_(zin, non_blocking=True)          # H2D: the step's input latent
+        eng.run(step_index(s), 1)
+        zout.copy_(eng.z.data, non_blocking=True)         # D2H: the step's result
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    assert torch.isfinite(zout).all(), "non-finite latent"
+
+    if rank != 0:
+        eng.close()
+        return
+    names = ["self_attention", "cross_attention", "gemm"]
+    kern = {names[i]: {"launches": int(nl[i]), "ms": kms[i], "tflops": (kfl[i] / kms[i] / 1e9) if kms[i] else None,
+                       "share_of_step": kms[i] / ms if ms else None} for i in range(3)}
+    dom = max(range(3), key=lambda i: kms[i])
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("bf16_tflops_sustained") or 1400.0
+    achieved = kfl[dom] / kms[dom] / 1e9 if kms[dom] else None
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = prof.get(names[dom], {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    # communication per video (50 steps): measured NCCL bytes, exact all-gather layout, reference ledger, NMP
+    per_step_nccl = (c1["nccl_bytes_received"] - c0["nccl_bytes_received"]) * world / args.steps
+    led = ag = 0
+    for i in range(1, T_SCHED + 1):
+        p = lp.build_plan(DIMS, PATCH, i, K, R_OVERLAP)
+        a, b = lp.step_comm_bytes(p, DIMS, 2, world, 4)
+        led += a
+        ag += b
+    tokens = (DIMS[1] // PATCH[0]) * (DIMS[2] // PATCH[1]) * (DIMS[3] // PATCH[2])
+    nmp = 2 * T_SCHED * (K - 1) * tokens * 1536 * 2
+    value = args.steps / (ms / 1000.0)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (synthetic_inputs seed 2025; random-init weights, pinned generator)",
+        "config": workload(K, world, args.layers),
+        "e2e": {"value": args.steps / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": zin.numel() * 4,
+                "d2h_bytes_per_step": zout.numel() * 4},
+        "gpu_launches": launches,
+        "roofline": {"bound": "tensor", "kernel": names[dom], "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if achieved else None, "traffic": traffic,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"},
+        "kernels": kern,
+        "clocks": clk.summary(),
+        "comm": {"nccl_bytes_per_step_measured_all_ranks": per_step_nccl,
+                 "allgather_bytes_per_video": ag, "reference_ledger_bytes_per_video": led,
+                 "reference_nmp_bytes_per_video": nmp, "wire": "f32 eps shards (ledger counts the 2-B preset width)"},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        v, info = cpu_reference_run(args.cpu_steps, K, os.cpu_count() or 1)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
+                                "sample": info["sample"]}
+    print(json.dumps(line), flush=True)
+    eng.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workers", type=int, default=0, help="LP workers K (default max(4, N))")
+    ap.add_argument("--layers", type=int, default=30)
+    ap.add_argument("--cpu-steps", type=int, default=24)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

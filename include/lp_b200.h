@@ -150,6 +150,11 @@ int lp_device_check(int device); /* LP_OK iff device exists and is sm_100 */
 int lp_device_flags(uint32_t* flags_out, int reset);
 /* Kernel launches issued by this library since load. */
 uint64_t lp_launch_count(void);
+/* Live per-kernel-class timing with CUDA events on the launching stream
+ * (classes: 0 self-attention, 1 cross-attention, 2 GEMM).  collect() fills 3
+ * entries each: launches, device ms, algorithmic FLOPs, algorithmic bytes. */
+int lp_profile_enable(int on);
+int lp_profile_collect(uint64_t* launches, double* ms, double* flops, double* bytes);
 
 /* K1: partition gather — extract_sublatents / slice_axis
  * (src/partition.cpp:136-148, src/latent.cpp:81-111).  Copies the entries

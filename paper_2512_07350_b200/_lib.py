@@ -86,6 +86,8 @@ _SIGS = {
     "lp_device_check": (_i, [_i]),
     "lp_device_flags": (_i, [C.POINTER(C.c_uint32), _i]),
     "lp_launch_count": (C.c_uint64, []),
+    "lp_profile_enable": (_i, [_i]),
+    "lp_profile_collect": (_i, [C.POINTER(C.c_uint64), _f64p, _f64p, _f64p]),
     "lp_extract": (_i, [_PlanP, _i32, _i32, _vp, _i64p, _i, _vp, _vp]),
     "lp_toy_predict": (_i, [_i32, _i64p, _d, _d, _vp, _i64p, _i, _i, _d, _vp, _vp]),
     "lp_toy_cfg_predict": (_i, [_i32, _i64p, _d, _d, _vp, _i64p, _i, _i, _d, _d, _vp, _vp, _vp]),

@@ -265,8 +265,12 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     a.ldo = x.ldo;
     a.scale_log2 = x.scale * 1.4426950408889634f;
     const dim3 grid(static_cast<unsigned>((x.n_q + kTile - 1) / kTile), x.heads, x.batch);
+    const int cls = x.n_kv == x.n_q && x.q == x.k ? KC_SELF_ATTN : KC_CROSS_ATTN;
+    prof_begin(cls, st);
     k_attention<<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a);
     LP_LAUNCH_CHECK();
+    prof_end(cls, st, 4.0 * x.batch * x.heads * static_cast<double>(x.n_q) * static_cast<double>(x.n_kv) * kHD,
+             2.0 * x.batch * x.heads * kHD * (2.0 * x.n_q + 2.0 * x.n_kv));
 }
 
 }  // namespace lpb200

@@ -64,6 +64,13 @@ inline void check_dtype(int d) {
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Optional per-kernel-class timing (CUDA events on the launching stream), used by
+// bench.py to measure the dominant kernel's live duration inside the timed region.
+enum KernelClass { KC_SELF_ATTN = 0, KC_CROSS_ATTN = 1, KC_GEMM = 2, KC_COUNT = 3 };
+bool prof_enabled();
+void prof_begin(int cls, cudaStream_t st);
+void prof_end(int cls, cudaStream_t st, double flops, double bytes);
+
 // Device-side sticky error word (NonFinite etc.), read by lp_device_flags().
 enum : unsigned { LP_FLAG_NONFINITE = 1u, LP_FLAG_ZERO_WEIGHT = 2u };
 unsigned* device_flags_ptr();  // current device's flag word

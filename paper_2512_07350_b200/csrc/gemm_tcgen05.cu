@@ -284,6 +284,7 @@ void gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int M, in
     if (M <= 0) return;
     if (K % 8 || lda % 8 || ldb % 8) fail(LP_ERR_INVALID_ARGUMENT, "gemm: K and strides must be multiples of 8");
     const CUtensorMap ta = make_tmap_2d_bf16(A, K, M, lda * 2, kBK, kBM);
+    prof_begin(KC_GEMM, st);
     switch (mode) {
         case EPI_BF16: gemm_bn<EPI_BF16>(ta, B, ldb, ep, M, N, K, st); break;
         case EPI_BF16_GELU: gemm_bn<EPI_BF16_GELU>(ta, B, ldb, ep, M, N, K, st); break;
@@ -291,6 +292,8 @@ void gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int M, in
         case EPI_F32: gemm_bn<EPI_F32>(ta, B, ldb, ep, M, N, K, st); break;
         default: fail(LP_ERR_INVALID_ARGUMENT, "gemm: bad epilogue");
     }
+    prof_end(KC_GEMM, st, 2.0 * M * N * K, 2.0 * (static_cast<double>(M) * K + static_cast<double>(N) * K) +
+                                               static_cast<double>(M) * N * (mode >= EPI_F32_RESID ? 4.0 : 2.0));
 }
 
 }  // namespace lpb200

@@ -168,9 +168,74 @@ double host_quantize(double v, int d) {
     return f16_decode_exact(f16_encode_exact(v));
 }
 
+namespace {
+struct ProfRec {
+    int cls;
+    cudaEvent_t a, b;
+    double flops, bytes;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_ev_pool;
+cudaEvent_t g_pending[KC_COUNT];
+cudaEvent_t take_event() {
+    if (!g_ev_pool.empty()) {
+        cudaEvent_t e = g_ev_pool.back();
+        g_ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    LP_CUDA(cudaEventCreate(&e));
+    return e;
+}
+}  // namespace
+
+bool prof_enabled() { return g_prof_on; }
+void prof_begin(int cls, cudaStream_t st) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_pending[cls] = take_event();
+    LP_CUDA(cudaEventRecord(g_pending[cls], st));
+}
+void prof_end(int cls, cudaStream_t st, double flops, double bytes) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEvent_t e = take_event();
+    LP_CUDA(cudaEventRecord(e, st));
+    g_prof.push_back({cls, g_pending[cls], e, flops, bytes});
+}
+
 }  // namespace lpb200
 
 using namespace lpb200;
+
+extern "C" int lp_profile_enable(int on) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        g_prof_on = on != 0;
+    });
+}
+
+// Per class: launches, summed device ms, summed algorithmic flops and bytes; clears.
+extern "C" int lp_profile_collect(uint64_t* launches, double* ms, double* flops, double* bytes) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        for (int c = 0; c < KC_COUNT; ++c) launches[c] = 0, ms[c] = 0, flops[c] = 0, bytes[c] = 0;
+        for (auto& r : g_prof) {
+            LP_CUDA(cudaEventSynchronize(r.b));
+            float t = 0.f;
+            LP_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+            launches[r.cls] += 1;
+            ms[r.cls] += t;
+            flops[r.cls] += r.flops;
+            bytes[r.cls] += r.bytes;
+            g_ev_pool.push_back(r.a);
+            g_ev_pool.push_back(r.b);
+        }
+        g_prof.clear();
+    });
+}
 
 extern "C" {
 

@@ -1,0 +1,80 @@
+"""Summarise ncu outputs into profiles/ (tracked):
+  - a launch list (--metrics gpu__time_duration.sum) -> per-kernel share of device time
+  - a --set full report -> per-kernel duration, DRAM bytes, tensor-pipe / MUFU / DRAM utilisation
+
+usage: python scripts/ncu_summary.py <launches.csv> <report.ncu-rep> <tag>
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+from collections import defaultdict
+
+
+def short(name):
+    return name.split("(")[0].replace("void ", "")
+
+
+def launches(path):
+    rows = list(csv.reader(l for l in open(path) if l.startswith('"')))
+    hdr = rows[0]
+    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    tot = defaultdict(float)
+    cnt = defaultdict(int)
+    for r in rows[1:]:
+        k = short(r[ki])
+        tot[k] += float(r[vi].replace(",", ""))
+        cnt[k] += 1
+    s = sum(tot.values())
+    return {k: {"launches": cnt[k], "ns": tot[k], "share": tot[k] / s} for k in sorted(tot, key=lambda x: -tot[x])}
+
+
+METRICS = {
+    "duration_ms": "gpu__time_duration.sum",
+    "dram_read_MB": "dram__bytes_read.sum",
+    "dram_write_MB": "dram__bytes_write.sum",
+    "tensor_pipe_active_pct": "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "mufu_xu_pct_active": "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "fma_pipe_pct_active": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "dram_throughput_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "smem_bank_conflicts": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "registers": "launch__registers_per_thread",
+}
+
+
+def full(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = {"kernel": short(r[hdr.index("Kernel Name")]), "grid": r[hdr.index("Grid Size")] if "Grid Size" in hdr else ""}
+        for k, m in METRICS.items():
+            if m in hdr:
+                v = r[hdr.index(m)].replace(",", "")
+                try:
+                    d[k] = float(v)
+                except ValueError:
+                    d[k] = v
+        res.append(d)
+    return res
+
+
+if __name__ == "__main__":
+    lpath, rpath, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+    os.makedirs("profiles", exist_ok=True)
+    summary = {"launch_list": launches(lpath) if os.path.exists(lpath) else {},
+               "full": full(rpath) if os.path.exists(rpath) else []}
+    json.dump(summary, open(f"profiles/{tag}_ncu.json", "w"), indent=1)
+    with open(f"profiles/{tag}_ncu.md", "w") as f:
+        f.write(f"# ncu summary — {tag}\n\n## Launch list (cold-cache, serialised; compare shares)\n\n")
+        f.write("| kernel | launches | total ms | share |\n|---|---|---|---|\n")
+        for k, v in summary["launch_list"].items():
+            f.write(f"| {k} | {v['launches']} | {v['ns'] / 1e6:.3f} | {100 * v['share']:.1f}% |\n")
+        f.write("\n## `--set full` captures\n\n| kernel | " + " | ".join(METRICS) + " |\n|" + "---|" * (len(METRICS) + 1) + "\n")
+        for d in summary["full"]:
+            f.write(f"| {d['kernel']} | " + " | ".join(str(d.get(k, "")) for k in METRICS) + " |\n")
+    print(open(f"profiles/{tag}_ncu.md").read())

@@ -1,14 +1,21 @@
 // attn_tcgen05.cu — FlashAttention-style forward on tcgen05 (sm_100a), head_dim 128.
 //
-// One CTA per (128-row Q tile, head, batch).  Roles (192 threads):
-//   warp 0      TMA producer: Q once, then K_j/V_j into a 2-stage ring
-//   warp 1      MMA issuer (one lane):  S_j = Q K_j^T  -> TMEM (double-buffered)
-//                                       O  += P_j V_j  -> TMEM
-//   warps 2..5  softmax: one thread per query row (its TMEM lane); online
-//               softmax in the exp2 domain with lazy rescaling (O is only
-//               rescaled when the running max grows by > 8, i.e. 2^8), P_j
-//               written to shared memory in the UMMA K-major 128B-swizzle layout.
-// V is consumed straight from its row-major [kv, d] tile as an MN-major B operand.
+// One CTA per (256 query rows = two 128-row Q tiles, head, batch).  Roles (320 threads):
+//   warp 0      TMA producer: Q0/Q1 once, then K_j/V_j into a 2-stage ring
+//   warp 1      MMA issuer (one lane), per kv block j and tile t in {0,1}:
+//                   S_t = Q_t K_j^T            (SS: both operands in smem)  -> TMEM
+//                   O_t += P_t V_j             (TS: P read from TMEM, V as MN-major smem)
+//               The two tiles ping-pong so the tensor pipe runs one tile's MMAs while
+//               the other tile's softmax runs.
+//   warps 2..5  softmax of tile 0, warps 6..9 softmax of tile 1: one thread per query
+//               row (its TMEM lane).  Online softmax in the exp2 domain with lazy
+//               rescaling (O only rescaled when the running max grows by more than 8,
+//               i.e. 2^8 headroom).  P_j is written back as packed bf16 into the first
+//               64 columns of S_t's own TMEM columns (no shared-memory round trip).
+// TMEM (512 columns): S0 [0,128), S1 [128,256), O0 [256,384), O1 [384,512).
+// Ordering: tcgen05 MMAs from one thread execute in issue order, so S_t(j+1), issued
+// after O_t += P_t(j) V_j, never overwrites P_t(j) early, and the s_full commit of
+// S_t(j+1) also certifies that O_t(j) is final before the softmax rescales it.
 #include <cuda.h>
 
 #include "dit_ops.hpp"
@@ -18,13 +25,12 @@ namespace lpb200 {
 
 using namespace tc;
 
-constexpr int kAttnThreads = 192;
-constexpr int kTile = 128;          // q rows and kv rows per block
-constexpr int kHD = 128;            // head dim
-constexpr int kAtom = 128 * 128;    // bytes of one [128 rows x 128 B] swizzle block
+constexpr int kAttnThreads = 320;
+constexpr int kTile = 128;             // q rows per tile and kv rows per block
+constexpr int kHD = 128;               // head dim
+constexpr int kAtom = 128 * 128;       // one [128 rows x 128 B] swizzle block
 constexpr int kTileBytes = 2 * kAtom;  // [128 x 128] bf16 = 32 KB
-constexpr int kKVStages = 2;
-constexpr int kAttnSmem = kTileBytes /*Q*/ + kKVStages * 2 * kTileBytes /*K,V*/ + kTileBytes /*P*/ + 1024 + 256;
+constexpr int kAttnSmem = 2 * kTileBytes /*Q0,Q1*/ + 2 * 2 * kTileBytes /*K,V x 2 stages*/ + 1024 + 256;
 
 struct AttnKernelArgs {
     int64_t q_col0, k_col0, v_col0;
@@ -45,18 +51,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 const __grid_constant__ CUtensorMap tv, AttnKernelArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;
-    uint8_t* sK = sQ + kTileBytes;                  // [stage]
-    uint8_t* sV = sK + kKVStages * kTileBytes;      // [stage]
-    uint8_t* sP = sV + kKVStages * kTileBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kTileBytes);
+    uint8_t* sQ = smem;                  // [tile][2 atoms]
+    uint8_t* sK = sQ + 2 * kTileBytes;   // [stage]
+    uint8_t* sV = sK + 2 * kTileBytes;   // [stage]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kTileBytes);
     uint64_t* q_full = bars + 0;
     uint64_t* kv_full = bars + 1;   // [2]
     uint64_t* kv_empty = bars + 3;  // [2]
-    uint64_t* s_full = bars + 5;    // [2]
-    uint64_t* s_empty = bars + 7;   // [2]
-    uint64_t* p_full = bars + 9;
-    uint64_t* o_done = bars + 10;
+    uint64_t* s_full = bars + 5;    // [tile]
+    uint64_t* p_full = bars + 7;    // [tile]
+    uint64_t* o_final = bars + 9;   // [tile]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
     const uint32_t warp = warp_id(), lane = lane_id();
@@ -72,10 +76,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             mbar_init(&kv_full[s], 1);
             mbar_init(&kv_empty[s], 1);
             mbar_init(&s_full[s], 1);
-            mbar_init(&s_empty[s], 128);
+            mbar_init(&p_full[s], 128);
+            mbar_init(&o_final[s], 1);
         }
-        mbar_init(p_full, 128);
-        mbar_init(o_done, 1);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -83,21 +86,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tS[2] = {tmem, tmem + 128};
-    const uint32_t tO = tmem + 256;
 
     if (warp == 0) {
         if (lane == 0) {
-            const int32_t qrow = static_cast<int32_t>(b * a.q_rows_per_batch + qt * kTile);
+            const int32_t qrow = static_cast<int32_t>(b * a.q_rows_per_batch + qt * 2 * kTile);
             const int32_t qc = static_cast<int32_t>(a.q_col0 + h * kHD);
-            mbar_arrive_expect_tx(q_full, kTileBytes);
-            tma_load_2d(&tq, q_full, sQ, qc, qrow);
-            tma_load_2d(&tq, q_full, sQ + kAtom, qc + 64, qrow);
+            mbar_arrive_expect_tx(q_full, 2 * kTileBytes);
+            for (int t = 0; t < 2; ++t) {
+                tma_load_2d(&tq, q_full, sQ + t * kTileBytes, qc, qrow + t * kTile);
+                tma_load_2d(&tq, q_full, sQ + t * kTileBytes + kAtom, qc + 64, qrow + t * kTile);
+            }
             const int32_t kc = static_cast<int32_t>(a.k_col0 + h * kHD), vc = static_cast<int32_t>(a.v_col0 + h * kHD);
             for (int j = 0; j < nkv; ++j) {
                 const int s = j & 1;
-                const uint32_t ph = (j >> 1) & 1;
-                mbar_wait(&kv_empty[s], ph ^ 1);
+                mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
                 mbar_arrive_expect_tx(&kv_full[s], 2 * kTileBytes);
                 const int32_t kr = static_cast<int32_t>(b * a.kv_rows_per_batch + j * kTile);
                 tma_load_2d(&tk, &kv_full[s], sK + s * kTileBytes, kc, kr);
@@ -110,124 +112,123 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         if (lane == 0) {
             constexpr uint32_t idS = idesc_bf16(128, 128);
             constexpr uint32_t idO = idesc_bf16(128, 128, /*b_mn_major=*/true);
-            const uint32_t q0 = smem_u32(sQ), p0 = smem_u32(sP);
             mbar_wait(q_full, 0);
-            auto issue_s = [&](int j) {
-                const int s = j & 1;
-                mbar_wait(&kv_full[s], (j >> 1) & 1);
-                if (j >= 2) mbar_wait(&s_empty[s], ((j - 2) >> 1) & 1);
-                tc_fence_after();
-                const uint32_t k0 = smem_u32(sK + s * kTileBytes);
+            auto issue_s = [&](int t, int j) {
+                const uint32_t q0 = smem_u32(sQ + t * kTileBytes), k0 = smem_u32(sK + (j & 1) * kTileBytes);
 #pragma unroll
                 for (int k = 0; k < kHD / 16; ++k) {
                     const uint32_t off = (k >> 2) * kAtom + (k & 3) * 32;
-                    mma_ss(tS[s], desc_sw128(q0 + off), desc_sw128(k0 + off), idS, k != 0);
+                    mma_ss(tmem + t * 128, desc_sw128(q0 + off), desc_sw128(k0 + off), idS, k != 0);
                 }
-                mma_commit(&s_full[s]);
+                mma_commit(&s_full[t]);
             };
-            issue_s(0);
-            for (int j = 0; j < nkv; ++j) {
-                const int s = j & 1;
-                if (j + 1 < nkv) issue_s(j + 1);
-                mbar_wait(p_full, j & 1);
-                tc_fence_after();
-                const uint32_t v0 = smem_u32(sV + s * kTileBytes);
+            auto issue_pv = [&](int t, int j) {
+                const uint32_t v0 = smem_u32(sV + (j & 1) * kTileBytes);
 #pragma unroll
                 for (int k = 0; k < kTile / 16; ++k) {
-                    // A = P (K-major, 2 atoms of 64 kv); B = V [kv][d] MN-major:
-                    // 16 kv rows per step (2048 B), the two 64-wide d halves LBO = 16 KB apart
-                    const uint64_t pd = desc_sw128(p0 + (k >> 2) * kAtom + (k & 3) * 32);
-                    const uint64_t vd = desc_sw128(v0 + k * 2048, /*sbo=*/1024, /*lbo=*/kAtom);
-                    mma_ss(tO, pd, vd, idO, (j | k) != 0);
+                    // A = P_t (TMEM, bf16 pairs: 8 columns per 16 kv); B = V [kv][d] MN-major:
+                    // 16 kv rows per step (2048 B), d halves LBO = 16 KB apart
+                    mma_ts(tmem + 256 + t * 128, tmem + t * 128 + k * 8,
+                           desc_sw128(v0 + k * 2048, /*sbo=*/1024, /*lbo=*/kAtom), idO, (j | k) != 0);
                 }
-                mma_commit(o_done);
-                mma_commit(&kv_empty[s]);
+            };
+            mbar_wait(&kv_full[0], 0);
+            tc_fence_after();
+            issue_s(0, 0);
+            issue_s(1, 0);
+            for (int j = 0; j < nkv; ++j) {
+                const bool more = j + 1 < nkv;
+                if (more) {
+                    mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+                }
+                for (int t = 0; t < 2; ++t) {
+                    mbar_wait(&p_full[t], j & 1);
+                    tc_fence_after();
+                    issue_pv(t, j);
+                    if (!more) mma_commit(&o_final[t]);
+                    if (t == 1) mma_commit(&kv_empty[j & 1]);
+                    if (more) issue_s(t, j + 1);
+                }
             }
         }
     } else {
-        // softmax warpgroup: thread <-> query row (TMEM lane)
+        // softmax warpgroups: tile t = (warp - 2) / 4, thread <-> query row / TMEM lane
+        const int t = (warp - 2) >> 2;
         const uint32_t q = warp & 3;
         const int row = q * 32 + lane;
         const uint32_t lane_off = (q * 32) << 16;
+        const uint32_t tS = tmem + t * 128 + lane_off, tO = tmem + 256 + t * 128 + lane_off;
+        const float c = a.scale_log2;
         float m_run = -INFINITY, l_run = 0.f;
         for (int j = 0; j < nkv; ++j) {
-            const int s = j & 1;
-            mbar_wait(&s_full[s], (j >> 1) & 1);
+            mbar_wait(&s_full[t], j & 1);
             tc_fence_after();
             float sv[kTile];
 #pragma unroll
-            for (int c = 0; c < kTile; c += 32) {
+            for (int cc = 0; cc < kTile; cc += 32) {
                 uint32_t r[32];
-                tmem_ld32(tS[s] + lane_off + c, r);
-                tmem_ld_wait();
+                tmem_ld32(tS + cc, r);
 #pragma unroll
-                for (int u = 0; u < 32; ++u) sv[c + u] = __uint_as_float(r[u]) * a.scale_log2;
+                for (int u = 0; u < 32; ++u) sv[cc + u] = __uint_as_float(r[u]);
             }
-            tc_fence_before();
-            mbar_arrive(&s_empty[s]);
+            tmem_ld_wait();
             const int valid = static_cast<int>(a.n_kv - static_cast<int64_t>(j) * kTile);
             if (valid < kTile) {
 #pragma unroll
                 for (int u = 0; u < kTile; ++u)
                     if (u >= valid) sv[u] = -INFINITY;
             }
-            float mx = m_run;
+            float mx = sv[0];
 #pragma unroll
-            for (int u = 0; u < kTile; ++u) mx = fmaxf(mx, sv[u]);
-            // lazy rescale: keep the stale max unless it grew by more than 8 (2^8 headroom)
-            const bool need = (mx > m_run + 8.f) || (m_run == -INFINITY);
-            float m_use = need ? mx : m_run;
-            const float alpha = need ? (m_run == -INFINITY ? 0.f : ex2(m_run - mx)) : 1.f;
-            // P_{j-1} consumed and O settled before P_j / rescale
-            if (j > 0) {
-                mbar_wait(o_done, (j - 1) & 1);
-                tc_fence_after();
-                if (__any_sync(0xffffffff, need && m_run != -INFINITY)) {
+            for (int u = 1; u < kTile; ++u) mx = fmaxf(mx, sv[u]);
+            // lazy rescale: keep the stale max unless it grew by more than 8 (log2 units)
+            const bool need = m_run == -INFINITY || (mx - m_run) * c > 8.f;
+            if (__any_sync(0xffffffff, need && m_run != -INFINITY)) {
+                // O_t(j-1) is final: S_t(j) was issued after it and has completed
+                const float alpha = need && m_run != -INFINITY ? ex2((m_run - mx) * c) : 1.f;
 #pragma unroll 1
-                    for (int c = 0; c < kHD; c += 16) {
-                        uint32_t r[16];
-                        tmem_ld16(tO + lane_off + c, r);
-                        tmem_ld_wait();
+                for (int cc = 0; cc < kHD; cc += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(tO + cc, r);
+                    tmem_ld_wait();
 #pragma unroll
-                        for (int u = 0; u < 16; ++u) r[u] = __float_as_uint(__uint_as_float(r[u]) * alpha);
-                        tmem_st16(tO + lane_off + c, r);
-                    }
-                    tmem_st_wait();
+                    for (int u = 0; u < 32; ++u) r[u] = __float_as_uint(__uint_as_float(r[u]) * alpha);
+                    tmem_st32(tO + cc, r);
                 }
+                l_run *= alpha;
             }
-            l_run *= alpha;
-            m_run = m_use;
-            // P = exp2(s - m) -> bf16, swizzled into sP
-            uint8_t* prow = sP + row * 128;
+            if (need) m_run = mx;
+            const float mc = m_run * c;
+            // P = exp2(s*c - m*c) -> packed bf16 into S_t's first 64 columns
 #pragma unroll
-            for (int c = 0; c < kTile / 8; ++c) {
-                float p[8];
+            for (int cc = 0; cc < kTile; cc += 32) {
+                uint32_t pk[16];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    p[u] = ex2(sv[c * 8 + u] - m_use);
-                    l_run += p[u];
+                for (int u = 0; u < 16; ++u) {
+                    const float p0 = ex2(fmaf(sv[cc + 2 * u], c, -mc));
+                    const float p1 = ex2(fmaf(sv[cc + 2 * u + 1], c, -mc));
+                    l_run += p0 + p1;
+                    pk[u] = pack_bf16(p0, p1);
                 }
-                const int atom = c >> 3, cc = c & 7;
-                *reinterpret_cast<uint4*>(prow + atom * kAtom + ((cc ^ (row & 7)) << 4)) =
-                    make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]), pack_bf16(p[6], p[7]));
+                tmem_st16(tS + cc / 2, pk);
             }
-            fence_proxy_async();
+            tmem_st_wait();
             tc_fence_before();
-            mbar_arrive(p_full);
+            mbar_arrive(&p_full[t]);
         }
-        // epilogue: O / l -> bf16
-        mbar_wait(o_done, (nkv - 1) & 1);
+        // epilogue: O_t / l -> bf16 rows
+        mbar_wait(&o_final[t], 0);
         tc_fence_after();
-        const int64_t grow = static_cast<int64_t>(qt) * kTile + row;
+        const int64_t grow = static_cast<int64_t>(qt) * 2 * kTile + t * kTile + row;
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
         __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.o) + (b * a.q_rows_per_batch + grow) * a.ldo + h * kHD;
 #pragma unroll 1
-        for (int c = 0; c < kHD; c += 32) {
+        for (int cc = 0; cc < kHD; cc += 32) {
             uint32_t r[32];
-            tmem_ld32(tO + lane_off + c, r);
+            tmem_ld32(tO + cc, r);
             tmem_ld_wait();
             if (grow < a.n_q) {
-                uint4* o4 = reinterpret_cast<uint4*>(orow + c);
+                uint4* o4 = reinterpret_cast<uint4*>(orow + cc);
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
                     o4[u] = make_uint4(pack_bf16(__uint_as_float(r[8 * u + 0]) * inv, __uint_as_float(r[8 * u + 1]) * inv),
@@ -264,7 +265,7 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     a.o = x.o;
     a.ldo = x.ldo;
     a.scale_log2 = x.scale * 1.4426950408889634f;
-    const dim3 grid(static_cast<unsigned>((x.n_q + kTile - 1) / kTile), x.heads, x.batch);
+    const dim3 grid(static_cast<unsigned>((x.n_q + 2 * kTile - 1) / (2 * kTile)), x.heads, x.batch);
     const int cls = x.n_kv == x.n_q && x.q == x.k ? KC_SELF_ATTN : KC_CROSS_ATTN;
     prof_begin(cls, st);
     k_attention<<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a);

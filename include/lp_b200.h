@@ -127,6 +127,9 @@ int lp_plan_offsets(const lp_plan* plan, const int64_t shape[4], int64_t* offset
  * elements it owns).  Rank r's slot holds its entries packed in worker order. */
 int lp_shard_layout(const lp_plan* plan, const int64_t shape[4], int world, int rank, int32_t* owned_out,
                     int32_t* n_owned_out, int64_t* slot_elems_out);
+/* Element offset of every entry's ε̂ shard inside the gathered buffer
+ * (world slots of slot_elems): the layout K10 reads after the all-gather. */
+int lp_shard_bases(const lp_plan* plan, const int64_t shape[4], int world, int64_t* base_out);
 
 /* Communication accounting — CommLedger + run_lp metering (src/cluster.cpp:27-73,
  * 186-209): the reference ledger bytes of step i (2 passes x (scatter+gather)

@@ -79,7 +79,8 @@ _SIGS = {
     "lp_weight_profile": (_i, [_PlanP, _i32, _f64p]),
     "lp_plan_offsets": (_i, [_PlanP, _i64p, _i64p]),
     "lp_shard_layout": (_i, [_PlanP, _i64p, _i, _i, C.POINTER(_i32), C.POINTER(_i32), _i64p]),
-    "lp_step_comm_bytes": (_i, [_PlanP, _i64p, _i, _i, _i, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "lp_shard_bases": (_i, [_PlanP, _i64p, _i, _i64p]),
+    "lp_step_comm_bytes":(_i, [_PlanP, _i64p, _i, _i, _i, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "lp_f16_encode": (C.c_uint16, [_d]),
     "lp_f16_decode": (_d, [C.c_uint16]),
     "lp_quantize": (_d, [_d, _i]),

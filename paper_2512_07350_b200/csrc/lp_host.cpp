@@ -311,6 +311,13 @@ int lp_shard_layout(const lp_plan* plan, const int64_t shape[4], int world, int 
     });
 }
 
+int lp_shard_bases(const lp_plan* plan, const int64_t shape[4], int world, int64_t* base_out) {
+    return guard([&] {
+        const ShardLayout L = shard_layout(*plan, Shape4::from(shape), world, 0);
+        for (size_t k = 0; k < L.base.size(); ++k) base_out[k] = L.base[k];
+    });
+}
+
 int lp_step_comm_bytes(const lp_plan* plan, const int64_t shape[4], int wire_bytes, int world, int dtype_bytes,
                        uint64_t* ledger_out, uint64_t* allgather_out) {
     return guard([&] {

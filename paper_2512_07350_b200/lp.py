@@ -214,6 +214,13 @@ def shard_layout(plan: PartitionPlan, dims, world: int, rank: int):
     return list(owned[: n.value]), int(slot.value)
 
 
+def shard_bases(plan: PartitionPlan, dims, world: int):
+    """Offsets (elements) of every entry's shard in the gathered buffer."""
+    out = (C.c_int64 * plan.workers)()
+    check(lib().lp_shard_bases(C.byref(plan.raw), i64arr(dims), world, out))
+    return list(out)
+
+
 def step_comm_bytes(plan: PartitionPlan, dims, wire_bytes: int, world: int, dtype_bytes: int):
     a, b = C.c_uint64(), C.c_uint64()
     check(lib().lp_step_comm_bytes(C.byref(plan.raw), i64arr(dims), wire_bytes, world, dtype_bytes, C.byref(a),

@@ -18,6 +18,8 @@
 // S_t(j+1) also certifies that O_t(j) is final before the softmax rescales it.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "dit_ops.hpp"
 #include "tc_ptx.cuh"
 
@@ -46,6 +48,19 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+// exp2 on the FMA pipe (FA4-style degree-3 polynomial on the fractional part,
+// exponent by integer add): relieves the MUFU pipe for a share of the columns.
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -127.f);
+    const float xi = floorf(x);
+    const float f = x - xi;
+    float p = fmaf(0.077119089663028717f, f, 0.227564036846160889f);
+    p = fmaf(p, f, 0.695146143436431885f);
+    p = fmaf(p, f, 1.0f);
+    return __int_as_float(__float_as_int(p) + (static_cast<int>(xi) << 23));
+}
+
+template <int POLY>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     k_attention(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                 const __grid_constant__ CUtensorMap tv, AttnKernelArgs a) {
@@ -205,8 +220,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 uint32_t pk[16];
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
-                    const float p0 = ex2(fmaf(sv[cc + 2 * u], c, -mc));
-                    const float p1 = ex2(fmaf(sv[cc + 2 * u + 1], c, -mc));
+                    const bool poly = POLY > 0 && (u % 4) < POLY;
+                    const float x0 = fmaf(sv[cc + 2 * u], c, -mc), x1 = fmaf(sv[cc + 2 * u + 1], c, -mc);
+                    const float p0 = poly ? ex2_poly(x0) : ex2(x0);
+                    const float p1 = poly ? ex2_poly(x1) : ex2(x1);
                     l_run += p0 + p1;
                     pk[u] = pack_bf16(p0, p1);
                 }
@@ -243,10 +260,22 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
+static int attn_poly() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("LP_ATTN_POLY");
+        v = e ? atoi(e) : 0;
+        if (v < 0 || v > 2) v = 0;
+    }
+    return v;
+}
+
 void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        LP_CUDA(cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         attr = true;
     }
     if ((x.ldq | x.ldk | x.ldv | x.ldo) % 8) fail(LP_ERR_INVALID_ARGUMENT, "attention: strides must be multiples of 8");
@@ -268,7 +297,11 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     const dim3 grid(static_cast<unsigned>((x.n_q + 2 * kTile - 1) / (2 * kTile)), x.heads, x.batch);
     const int cls = x.n_kv == x.n_q && x.q == x.k ? KC_SELF_ATTN : KC_CROSS_ATTN;
     prof_begin(cls, st);
-    k_attention<<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a);
+    switch (attn_poly()) {
+        case 0: k_attention<0><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
+        case 2: k_attention<2><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
+        default: k_attention<1><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
+    }
     LP_LAUNCH_CHECK();
     prof_end(cls, st, 4.0 * x.batch * x.heads * static_cast<double>(x.n_q) * static_cast<double>(x.n_kv) * kHD,
              2.0 * x.batch * x.heads * kHD * (2.0 * x.n_q + 2.0 * x.n_kv));

@@ -17,6 +17,7 @@
 //   F32        out_f32  = acc + bias                      (head)
 #include <cuda.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -92,6 +93,43 @@ __device__ __forceinline__ float gelu_tanh(float x) {
     float t;
     asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
     return 0.5f * x * (1.f + t);
+}
+
+// one thread's 32 accumulator columns of row `row` -> fused epilogue store
+template <int MODE>
+__device__ __forceinline__ void epilogue_store(const GemmEpilogue& ep, int row, int col0, const uint32_t (&r)[32]) {
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + (ep.bias ? __ldg(ep.bias + col0 + j) : 0.f);
+    if (MODE == EPI_BF16 || MODE == EPI_BF16_GELU) {
+        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + col0;
+        uint4* o4 = reinterpret_cast<uint4*>(o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float a[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] = MODE == EPI_BF16_GELU ? gelu_tanh(v[8 * j + u]) : v[8 * j + u];
+            o4[j] = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
+        }
+    } else {
+        float* o = static_cast<float*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + col0;
+        float4* o4 = reinterpret_cast<float4*>(o);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float4 x;
+            if (MODE == EPI_F32_RESID) {
+                x = o4[j];
+                const float* g = ep.gate ? ep.gate + col0 + 4 * j : nullptr;
+                x.x += v[4 * j + 0] * (g ? __ldg(g + 0) : 1.f);
+                x.y += v[4 * j + 1] * (g ? __ldg(g + 1) : 1.f);
+                x.z += v[4 * j + 2] * (g ? __ldg(g + 2) : 1.f);
+                x.w += v[4 * j + 3] * (g ? __ldg(g + 3) : 1.f);
+            } else {
+                x = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
+            o4[j] = x;
+        }
+    }
 }
 
 template <int BN, int MODE>
@@ -189,42 +227,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 uint32_t r[32];
                 tmem_ld32(taddr + c, r);
                 tmem_ld_wait();
-                if (row < M) {
-                    const int col0 = nb * BN + c;
-                    float v[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + (ep.bias ? __ldg(ep.bias + col0 + j) : 0.f);
-                    if (MODE == EPI_BF16 || MODE == EPI_BF16_GELU) {
-                        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + col0;
-                        uint4* o4 = reinterpret_cast<uint4*>(o);
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            float a[8];
-#pragma unroll
-                            for (int u = 0; u < 8; ++u) a[u] = MODE == EPI_BF16_GELU ? gelu_tanh(v[8 * j + u]) : v[8 * j + u];
-                            o4[j] = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]),
-                                               pack_bf16(a[6], a[7]));
-                        }
-                    } else {
-                        float* o = static_cast<float*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + col0;
-                        float4* o4 = reinterpret_cast<float4*>(o);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            float4 x;
-                            if (MODE == EPI_F32_RESID) {
-                                x = o4[j];
-                                const float* g = ep.gate ? ep.gate + col0 + 4 * j : nullptr;
-                                x.x += v[4 * j + 0] * (g ? __ldg(g + 0) : 1.f);
-                                x.y += v[4 * j + 1] * (g ? __ldg(g + 1) : 1.f);
-                                x.z += v[4 * j + 2] * (g ? __ldg(g + 2) : 1.f);
-                                x.w += v[4 * j + 3] * (g ? __ldg(g + 3) : 1.f);
-                            } else {
-                                x = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                            }
-                            o4[j] = x;
-                        }
-                    }
-                }
+                if (row < M) epilogue_store<MODE>(ep, row, nb * BN + c, r);
             }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
@@ -232,6 +235,128 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     __syncthreads();
     if (warp == 2) tmem_dealloc(tmem, 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512))));
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a 2-CTA cluster computes a 256 x BN tile with
+// one UMMA_M = 256 instruction stream issued by the leader CTA.  Each CTA TMA-loads
+// its own 128 rows of A and BN/2 rows of B (half the B bytes per SM of the 1-CTA
+// kernel), both CTAs' loads complete on the leader's full barrier, and commits are
+// multicast to both CTAs.  Each CTA's TMEM holds its 128 accumulator rows.
+// ---------------------------------------------------------------------------
+template <int BN>
+constexpr int gemm2_stages() { return BN == 256 ? 6 : 8; }
+template <int BN>
+constexpr int gemm2_smem_bytes() {
+    return gemm2_stages<BN>() * (kBM * kBK * 2 + (BN / 2) * kBK * 2) + 1024 + 256;
+}
+
+template <int BN, int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    k_gemm2(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, GemmEpilogue ep, int M,
+            int N, int K) {
+    constexpr int S = gemm2_stages<BN>();
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int A_BYTES = kBM * kBK * 2, B_BYTES = (BN / 2) * kBK * 2;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + S * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * B_BYTES);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const uint32_t rank = cluster_ctarank();
+    const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+    const int num_n = N / BN, num_m = (M + 2 * kBM - 1) / (2 * kBM), tiles = num_m * num_n;
+    const int nk = (K + kBK - 1) / kBK;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tma);
+        tma_prefetch(&tmb);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 256);  // both CTAs' epilogue threads arrive on the leader's
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc_2sm(tmem_slot, 2 * BN);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = cluster; t < tiles; t += nclusters) {
+                const int mb = t / num_n, nb = t % num_n;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
+                    tma_load_2d_2sm(&tma, &full[s], sA + s * A_BYTES, kb * kBK, mb * 2 * kBM + rank * kBM);
+                    tma_load_2d_2sm(&tmb, &full[s], sB + s * B_BYTES, kb * kBK, nb * BN + rank * (BN / 2));
+                    if (++s == S) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = idesc_bf16(2 * kBM, BN);
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (int t = cluster; t < tiles; t += nclusters, ++it) {
+                const int acc = it & 1;
+                const uint32_t aph = (it >> 1) & 1;
+                mbar_wait(&tempty[acc], aph ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k)
+                        mma_ss_2sm(d, desc_sw128(a0 + k * 32), desc_sw128(b0 + k * 32), idesc, (kb | k) != 0);
+                    mma_commit_2sm(&empty[s], 0x3);
+                    if (++s == S) { s = 0; ph ^= 1; }
+                }
+                mma_commit_2sm(&tfull[acc], 0x3);
+            }
+        }
+    } else {
+        const uint32_t q = warp & 3;
+        int it = 0;
+        for (int t = cluster; t < tiles; t += nclusters, ++it) {
+            const int mb = t / num_n, nb = t % num_n;
+            const int acc = it & 1;
+            const uint32_t aph = (it >> 1) & 1;
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            const int row = mb * 2 * kBM + rank * kBM + q * 32 + lane;
+            const uint32_t taddr = tmem + ((q * 32) << 16) + acc * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t r[32];
+                tmem_ld32(taddr + c, r);
+                tmem_ld_wait();
+                if (row < M) epilogue_store<MODE>(ep, row, nb * BN + c, r);
+            }
+            tc_fence_before();
+            mbar_arrive_cluster(&tempty[acc], 0);
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 2) tmem_dealloc_2sm(tmem, 2 * BN);
 }
 
 // ---------------------------------------------------------------------------
@@ -262,9 +387,43 @@ static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Gemm
     LP_LAUNCH_CHECK();
 }
 
+template <int BN, int MODE>
+static void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmEpilogue& ep, int M, int N, int K,
+                         cudaStream_t st) {
+    constexpr int smem = gemm2_smem_bytes<BN>();
+    static bool attr = false;
+    if (!attr) {
+        LP_CUDA(cudaFuncSetAttribute(k_gemm2<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * (N / BN);
+    const int clusters = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+    k_gemm2<BN, MODE><<<2 * clusters, kGemmThreads, smem, st>>>(ta, tb, ep, M, N, K);
+    LP_LAUNCH_CHECK();
+}
+
+static int gemm_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("LP_GEMM_2SM");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
 template <int MODE>
 static void gemm_bn(const CUtensorMap& ta, const void* B, int64_t ldb, const GemmEpilogue& ep, int M, int N, int K,
                     cudaStream_t st) {
+    if (gemm_variant() && M > kBM && (N % 256 == 0 || N % 128 == 0)) {
+        if (N % 256 == 0) {
+            const CUtensorMap tb = make_tmap_2d_bf16(B, K, N, ldb * 2, kBK, 128);
+            launch_gemm2<256, MODE>(ta, tb, ep, M, N, K, st);
+        } else {
+            const CUtensorMap tb = make_tmap_2d_bf16(B, K, N, ldb * 2, kBK, 64);
+            launch_gemm2<128, MODE>(ta, tb, ep, M, N, K, st);
+        }
+        return;
+    }
     if (N % 256 == 0) {
         const CUtensorMap tb = make_tmap_2d_bf16(B, K, N, ldb * 2, kBK, 256);
         launch_gemm<256, MODE>(ta, tb, ep, M, N, K, st);

@@ -2,6 +2,7 @@
 DiT's shapes and attention at the C2 shard sizes.  Prints TFLOP/s per shape."""
 import ctypes as C
 import json
+import os
 import sys
 
 import torch
@@ -32,8 +33,9 @@ def timeit(fn, reps=10):
 
 out = {}
 R = 2 * 32760
-for (M, N, K, name) in [(R, 4608, 1536, "qkv"), (R, 1536, 1536, "o"), (R, 8960, 1536, "ffn1"), (R, 1536, 8960, "ffn2"),
-                        (8192, 8192, 8192, "sq8k")]:
+GEMMS = [(R, 4608, 1536, "qkv"), (R, 1536, 1536, "o"), (R, 8960, 1536, "ffn1"), (R, 1536, 8960, "ffn2"),
+         (8192, 8192, 8192, "sq8k")]
+for (M, N, K, name) in ([] if "attn" in sys.argv else GEMMS):
     A = torch.randn(M, K, device="cuda").bfloat16()
     B = torch.randn(N, K, device="cuda").bfloat16()
     D = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
@@ -45,7 +47,7 @@ for (M, N, K, name) in [(R, 4608, 1536, "qkv"), (R, 1536, 1536, "o"), (R, 8960, 
                            "cublas_ms": tc, "cublas_tflops": 2 * M * N * K / tc / 1e9}
     print(json.dumps({f"gemm_{name}": out[f"gemm_{name}"]}), flush=True)
     del A, B, D
-for (S, name) in [(32760, "self_k1"), (18720, "self_k4max"), (14040, "self_k4min")]:
+for (S, name) in ([] if "gemm" in sys.argv else [(32760, "self_k1"), (18720, "self_k4max"), (14040, "self_k4min")]):
     q = torch.randn(2, S, 12, 128, device="cuda").bfloat16()
     k = torch.randn(2, S, 12, 128, device="cuda").bfloat16()
     v = torch.randn(2, S, 12, 128, device="cuda").bfloat16()
@@ -59,4 +61,5 @@ for (S, name) in [(32760, "self_k1"), (18720, "self_k4max"), (14040, "self_k4min
     tsd = timeit(lambda: torch.nn.functional.scaled_dot_product_attention(qt, kt, vt), 5)
     out[f"attn_{name}"] = {"S": S, "ms": ms, "tflops": fl / ms / 1e9, "sdpa_ms": tsd, "sdpa_tflops": fl / tsd / 1e9}
     print(json.dumps({f"attn_{name}": out[f"attn_{name}"]}), flush=True)
-json.dump(out, open("gpurun_out/kbench.json", "w"), indent=1)
+tag = os.environ.get("KB_TAG", "")
+json.dump(out, open(f"gpurun_out/kbench{tag}.json", "w"), indent=1)

@@ -157,6 +157,9 @@ uint64_t lp_launch_count(void);
  * (classes: 0 self-attention, 1 cross-attention, 2 GEMM).  collect() fills 3
  * entries each: launches, device ms, algorithmic FLOPs, algorithmic bytes. */
 int lp_profile_enable(int on);
+/* Kernel-variant knobs (benchmarking): "attn_poly" (0-3: eighths of exp2 on the
+ * FMA pipe), "gemm_2sm" (0/1: CTA-pair GEMM).  Also read from LP_TUNE_<KEY>. */
+int lp_tune(const char* key, int value);
 int lp_profile_collect(uint64_t* launches, double* ms, double* flops, double* bytes);
 
 /* K1: partition gather — extract_sublatents / slice_axis
@@ -230,6 +233,11 @@ int lp_dit_create(const lp_dit_config* cfg, const double* cond_values, int32_t n
 int lp_dit_destroy(lp_dit* dit);
 /* Workspace for shards up to max_tokens tokens (allocates; call once). */
 int lp_dit_reserve(lp_dit* dit, int64_t max_tokens);
+/* Independent workspaces ("slots") so that several shards' forwards can be in
+ * flight at once on different streams (the engine overlaps its owned entries). */
+int lp_dit_reserve_slots(lp_dit* dit, int64_t max_tokens, int32_t nslots);
+int lp_dit_cfg_predict_slot(lp_dit* dit, int32_t slot, const void* sub, const int64_t shape[4], int dtype_bytes,
+                            int timestep, double guidance, void* eps_out, void* stream);
 /* cfg_predict with the DiT: CFG batch 2 (uncond = null text, cond = synthetic
  * text), one forward, combine uncond + w*(cond-uncond), quantize to dtype. */
 int lp_dit_cfg_predict(lp_dit* dit, const void* sub, const int64_t shape[4], int dtype_bytes, int timestep,

@@ -88,6 +88,7 @@ _SIGS = {
     "lp_device_flags": (_i, [C.POINTER(C.c_uint32), _i]),
     "lp_launch_count": (C.c_uint64, []),
     "lp_profile_enable": (_i, [_i]),
+    "lp_tune": (_i, [C.c_char_p, _i]),
     "lp_profile_collect": (_i, [C.POINTER(C.c_uint64), _f64p, _f64p, _f64p]),
     "lp_extract": (_i, [_PlanP, _i32, _i32, _vp, _i64p, _i, _vp, _vp]),
     "lp_toy_predict": (_i, [_i32, _i64p, _d, _d, _vp, _i64p, _i, _i, _d, _vp, _vp]),
@@ -103,6 +104,8 @@ _SIGS = {
     "lp_dit_destroy": (_i, [_vp]),
     "lp_dit_reserve": (_i, [_vp, _i64]),
     "lp_dit_cfg_predict": (_i, [_vp, _vp, _i64p, _i, _i, _d, _vp, _vp]),
+    "lp_dit_reserve_slots": (_i, [_vp, _i64, _i32]),
+    "lp_dit_cfg_predict_slot": (_i, [_vp, _i32, _vp, _i64p, _i, _i, _d, _vp, _vp]),
     "lp_dit_num_params": (_i, [_vp]),
     "lp_dit_param": (_i, [_vp, _i32, C.POINTER(C.c_char_p), C.POINTER(_vp), _i64p, C.POINTER(_i32)]),
     "lp_dit_debug_tensor": (_i, [_vp, C.c_char_p, C.POINTER(_vp), _i64p]),

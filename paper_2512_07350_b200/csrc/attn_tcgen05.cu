@@ -32,7 +32,8 @@ constexpr int kTile = 128;             // q rows per tile and kv rows per block
 constexpr int kHD = 128;               // head dim
 constexpr int kAtom = 128 * 128;       // one [128 rows x 128 B] swizzle block
 constexpr int kTileBytes = 2 * kAtom;  // [128 x 128] bf16 = 32 KB
-constexpr int kAttnSmem = 2 * kTileBytes /*Q0,Q1*/ + 2 * 2 * kTileBytes /*K,V x 2 stages*/ + 1024 + 256;
+constexpr int kKStages = 3, kVStages = 2;
+constexpr int kAttnSmem = (2 /*Q0,Q1*/ + kKStages + kVStages) * kTileBytes + 1024 + 256;
 
 struct AttnKernelArgs {
     int64_t q_col0, k_col0, v_col0;
@@ -50,14 +51,19 @@ __device__ __forceinline__ float ex2(float x) {
 
 // exp2 on the FMA pipe (FA4-style degree-3 polynomial on the fractional part,
 // exponent by integer add): relieves the MUFU pipe for a share of the columns.
+// Only FMA/ALU-pipe instructions (no FRND/F2I, which share the MUFU/XU pipe):
+// round-to-nearest via the 1.5*2^23 magic constant, f in [-0.5, 0.5], degree-4
+// polynomial for 2^f (rel. error < 2e-5, far below bf16's 4e-3), exponent added
+// as an integer shift.
 __device__ __forceinline__ float ex2_poly(float x) {
-    x = fmaxf(x, -127.f);
-    const float xi = floorf(x);
-    const float f = x - xi;
-    float p = fmaf(0.077119089663028717f, f, 0.227564036846160889f);
-    p = fmaf(p, f, 0.695146143436431885f);
+    x = fmaxf(x, -126.f);
+    const float t = x + 12582912.f;   // 1.5 * 2^23: integer part lands in the low mantissa bits
+    const float f = x - (t - 12582912.f);
+    float p = fmaf(0.0096181291f, f, 0.0555041087f);
+    p = fmaf(p, f, 0.2402265070f);
+    p = fmaf(p, f, 0.6931471806f);
     p = fmaf(p, f, 1.0f);
-    return __int_as_float(__float_as_int(p) + (static_cast<int>(xi) << 23));
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
 template <int POLY>
@@ -66,17 +72,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 const __grid_constant__ CUtensorMap tv, AttnKernelArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;                  // [tile][2 atoms]
-    uint8_t* sK = sQ + 2 * kTileBytes;   // [stage]
-    uint8_t* sV = sK + 2 * kTileBytes;   // [stage]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kTileBytes);
+    uint8_t* sQ = smem;                          // [tile][2 atoms]
+    uint8_t* sK = sQ + 2 * kTileBytes;           // [kKStages]
+    uint8_t* sV = sK + kKStages * kTileBytes;    // [kVStages]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVStages * kTileBytes);
     uint64_t* q_full = bars + 0;
-    uint64_t* kv_full = bars + 1;   // [2]
-    uint64_t* kv_empty = bars + 3;  // [2]
-    uint64_t* s_full = bars + 5;    // [tile]
-    uint64_t* p_full = bars + 7;    // [tile]
-    uint64_t* o_final = bars + 9;   // [tile]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+    uint64_t* k_full = bars + 1;    // [kKStages]
+    uint64_t* k_empty = bars + 4;   // [kKStages]
+    uint64_t* v_full = bars + 7;    // [kVStages]
+    uint64_t* v_empty = bars + 9;   // [kVStages]
+    uint64_t* s_full = bars + 11;   // [tile]
+    uint64_t* p_full = bars + 13;   // [tile]
+    uint64_t* p_half = bars + 15;   // [tile]
+    uint64_t* o_final = bars + 17;  // [tile]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
 
     const uint32_t warp = warp_id(), lane = lane_id();
     const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -87,11 +96,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tma_prefetch(&tk);
         tma_prefetch(&tv);
         mbar_init(q_full, 1);
+        for (int s = 0; s < kKStages; ++s) {
+            mbar_init(&k_full[s], 1);
+            mbar_init(&k_empty[s], 1);
+        }
+        for (int s = 0; s < kVStages; ++s) {
+            mbar_init(&v_full[s], 1);
+            mbar_init(&v_empty[s], 1);
+        }
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&kv_full[s], 1);
-            mbar_init(&kv_empty[s], 1);
             mbar_init(&s_full[s], 1);
             mbar_init(&p_full[s], 128);
+            mbar_init(&p_half[s], 128);
             mbar_init(&o_final[s], 1);
         }
         fence_barrier_init();
@@ -104,6 +120,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {
+            // K runs ahead in a 3-deep ring (needed first, by S = Q K^T); V in a 2-deep ring
             const int32_t qrow = static_cast<int32_t>(b * a.q_rows_per_batch + qt * 2 * kTile);
             const int32_t qc = static_cast<int32_t>(a.q_col0 + h * kHD);
             mbar_arrive_expect_tx(q_full, 2 * kTileBytes);
@@ -112,15 +129,27 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 tma_load_2d(&tq, q_full, sQ + t * kTileBytes + kAtom, qc + 64, qrow + t * kTile);
             }
             const int32_t kc = static_cast<int32_t>(a.k_col0 + h * kHD), vc = static_cast<int32_t>(a.v_col0 + h * kHD);
-            for (int j = 0; j < nkv; ++j) {
-                const int s = j & 1;
-                mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&kv_full[s], 2 * kTileBytes);
+            auto load_k = [&](int j) {
+                const int s = j % kKStages;
+                mbar_wait(&k_empty[s], ((j / kKStages) & 1) ^ 1);
+                mbar_arrive_expect_tx(&k_full[s], kTileBytes);
                 const int32_t kr = static_cast<int32_t>(b * a.kv_rows_per_batch + j * kTile);
-                tma_load_2d(&tk, &kv_full[s], sK + s * kTileBytes, kc, kr);
-                tma_load_2d(&tk, &kv_full[s], sK + s * kTileBytes + kAtom, kc + 64, kr);
-                tma_load_2d(&tv, &kv_full[s], sV + s * kTileBytes, vc, kr);
-                tma_load_2d(&tv, &kv_full[s], sV + s * kTileBytes + kAtom, vc + 64, kr);
+                tma_load_2d(&tk, &k_full[s], sK + s * kTileBytes, kc, kr);
+                tma_load_2d(&tk, &k_full[s], sK + s * kTileBytes + kAtom, kc + 64, kr);
+            };
+            auto load_v = [&](int j) {
+                const int s = j % kVStages;
+                mbar_wait(&v_empty[s], ((j / kVStages) & 1) ^ 1);
+                mbar_arrive_expect_tx(&v_full[s], kTileBytes);
+                const int32_t kr = static_cast<int32_t>(b * a.kv_rows_per_batch + j * kTile);
+                tma_load_2d(&tv, &v_full[s], sV + s * kTileBytes, vc, kr);
+                tma_load_2d(&tv, &v_full[s], sV + s * kTileBytes + kAtom, vc + 64, kr);
+            };
+            int jk = 0;
+            for (; jk < nkv && jk < kKStages - 1; ++jk) load_k(jk);
+            for (int j = 0; j < nkv; ++j) {
+                load_v(j);
+                if (jk < nkv) load_k(jk++);
             }
         }
     } else if (warp == 1) {
@@ -129,39 +158,44 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             constexpr uint32_t idO = idesc_bf16(128, 128, /*b_mn_major=*/true);
             mbar_wait(q_full, 0);
             auto issue_s = [&](int t, int j) {
-                const uint32_t q0 = smem_u32(sQ + t * kTileBytes), k0 = smem_u32(sK + (j & 1) * kTileBytes);
+                const int s = j % kKStages;
+                if (t == 0) {
+                    mbar_wait(&k_full[s], (j / kKStages) & 1);
+                    tc_fence_after();
+                }
+                const uint32_t q0 = smem_u32(sQ + t * kTileBytes), k0 = smem_u32(sK + s * kTileBytes);
 #pragma unroll
                 for (int k = 0; k < kHD / 16; ++k) {
                     const uint32_t off = (k >> 2) * kAtom + (k & 3) * 32;
                     mma_ss(tmem + t * 128, desc_sw128(q0 + off), desc_sw128(k0 + off), idS, k != 0);
                 }
                 mma_commit(&s_full[t]);
+                if (t == 1) mma_commit(&k_empty[s]);  // both tiles' S issued: K_j slot frees on completion
             };
-            auto issue_pv = [&](int t, int j) {
-                const uint32_t v0 = smem_u32(sV + (j & 1) * kTileBytes);
+            auto issue_pv = [&](int t, int j, int half) {
+                const uint32_t v0 = smem_u32(sV + (j % kVStages) * kTileBytes);
 #pragma unroll
-                for (int k = 0; k < kTile / 16; ++k) {
+                for (int k = half * 4; k < half * 4 + 4; ++k) {
                     // A = P_t (TMEM, bf16 pairs: 8 columns per 16 kv); B = V [kv][d] MN-major:
                     // 16 kv rows per step (2048 B), d halves LBO = 16 KB apart
                     mma_ts(tmem + 256 + t * 128, tmem + t * 128 + k * 8,
                            desc_sw128(v0 + k * 2048, /*sbo=*/1024, /*lbo=*/kAtom), idO, (j | k) != 0);
                 }
             };
-            mbar_wait(&kv_full[0], 0);
-            tc_fence_after();
             issue_s(0, 0);
             issue_s(1, 0);
             for (int j = 0; j < nkv; ++j) {
                 const bool more = j + 1 < nkv;
-                if (more) {
-                    mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-                }
                 for (int t = 0; t < 2; ++t) {
+                    mbar_wait(&p_half[t], j & 1);
+                    if (t == 0) mbar_wait(&v_full[j % kVStages], (j / kVStages) & 1);
+                    tc_fence_after();
+                    issue_pv(t, j, 0);
                     mbar_wait(&p_full[t], j & 1);
                     tc_fence_after();
-                    issue_pv(t, j);
+                    issue_pv(t, j, 1);
                     if (!more) mma_commit(&o_final[t]);
-                    if (t == 1) mma_commit(&kv_empty[j & 1]);
+                    if (t == 1) mma_commit(&v_empty[j % kVStages]);
                     if (more) issue_s(t, j + 1);
                 }
             }
@@ -193,9 +227,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 for (int u = 0; u < kTile; ++u)
                     if (u >= valid) sv[u] = -INFINITY;
             }
-            float mx = sv[0];
+            // row max as an 8-way tree (a 127-long FMNMX chain is pure latency)
+            float m8[8];
 #pragma unroll
-            for (int u = 1; u < kTile; ++u) mx = fmaxf(mx, sv[u]);
+            for (int u = 0; u < 8; ++u) m8[u] = sv[u];
+#pragma unroll
+            for (int u = 8; u < kTile; ++u) m8[u & 7] = fmaxf(m8[u & 7], sv[u]);
+            const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                   fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
             // lazy rescale: keep the stale max unless it grew by more than 8 (log2 units)
             const bool need = m_run == -INFINITY || (mx - m_run) * c > 8.f;
             if (__any_sync(0xffffffff, need && m_run != -INFINITY)) {
@@ -214,24 +253,30 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             }
             if (need) m_run = mx;
             const float mc = m_run * c;
+            float lsum[4] = {0.f, 0.f, 0.f, 0.f};
             // P = exp2(s*c - m*c) -> packed bf16 into S_t's first 64 columns
+            // published in two halves: the MMA warp starts O += P[:, :64] V[:64] while the
+            // second half of the exponentials is still being computed
 #pragma unroll
             for (int cc = 0; cc < kTile; cc += 32) {
                 uint32_t pk[16];
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
-                    const bool poly = POLY > 0 && (u % 4) < POLY;
+                    const bool poly = POLY > 0 && (u % 8) < POLY;
                     const float x0 = fmaf(sv[cc + 2 * u], c, -mc), x1 = fmaf(sv[cc + 2 * u + 1], c, -mc);
                     const float p0 = poly ? ex2_poly(x0) : ex2(x0);
                     const float p1 = poly ? ex2_poly(x1) : ex2(x1);
-                    l_run += p0 + p1;
+                    lsum[u & 3] += p0 + p1;  // 4 independent partial sums
                     pk[u] = pack_bf16(p0, p1);
                 }
                 tmem_st16(tS + cc / 2, pk);
+                if (cc == 32 || cc == 96) {
+                    tmem_st_wait();
+                    tc_fence_before();
+                    mbar_arrive(cc == 32 ? &p_half[t] : &p_full[t]);
+                }
             }
-            tmem_st_wait();
-            tc_fence_before();
-            mbar_arrive(&p_full[t]);
+            l_run += (lsum[0] + lsum[1]) + (lsum[2] + lsum[3]);
         }
         // epilogue: O_t / l -> bf16 rows
         mbar_wait(&o_final[t], 0);
@@ -261,13 +306,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 }
 
 static int attn_poly() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("LP_ATTN_POLY");
-        v = e ? atoi(e) : 0;
-        if (v < 0 || v > 2) v = 0;
-    }
-    return v;
+    const int v = tune_get("attn_poly", 0);  // eighths of the exponentials on the FMA pipe (A/B: 0 best)
+    return v < 0 || v > 3 ? 0 : v;
 }
 
 void attention_bf16(const AttnArgs& x, cudaStream_t st) {
@@ -276,6 +316,7 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
         LP_CUDA(cudaFuncSetAttribute(k_attention<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         LP_CUDA(cudaFuncSetAttribute(k_attention<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         LP_CUDA(cudaFuncSetAttribute(k_attention<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         attr = true;
     }
     if ((x.ldq | x.ldk | x.ldv | x.ldo) % 8) fail(LP_ERR_INVALID_ARGUMENT, "attention: strides must be multiples of 8");
@@ -300,6 +341,7 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     switch (attn_poly()) {
         case 0: k_attention<0><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
         case 2: k_attention<2><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
+        case 3: k_attention<3><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
         default: k_attention<1><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
     }
     LP_LAUNCH_CHECK();

@@ -71,6 +71,9 @@ bool prof_enabled();
 void prof_begin(int cls, cudaStream_t st);
 void prof_end(int cls, cudaStream_t st, double flops, double bytes);
 
+// Tuning knobs (kernel variants), set via lp_tune() or LP_TUNE_<KEY> env vars.
+int tune_get(const char* key, int dflt);
+
 // Device-side sticky error word (NonFinite etc.), read by lp_device_flags().
 enum : unsigned { LP_FLAG_NONFINITE = 1u, LP_FLAG_ZERO_WEIGHT = 2u };
 unsigned* device_flags_ptr();  // current device's flag word

@@ -39,8 +39,13 @@ struct lp_engine {
     ReconParams recon[3];
     void* z = nullptr;
     void* gather = nullptr;
-    void* sub = nullptr;
+    void* sub = nullptr;  // [nslots][max_entry]
     double* ws = nullptr;
+    // owned entries' DiT forwards overlap on nslots streams (world == 1: K shards on one GPU)
+    int nslots = 1;
+    size_t sub_stride = 0;
+    cudaStream_t slot_stream[4] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join[4] = {};
     ncclComm_t comm = nullptr;
     uint64_t nccl_bytes = 0, ledger_bytes = 0, launches = 0;
 };
@@ -90,7 +95,17 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
             LP_CUDA(cudaMalloc(&e->z, static_cast<size_t>(e->shape.volume()) * E));
             LP_CUDA(cudaMalloc(&e->gather, static_cast<size_t>(max_slot) * c->world * E));
             LP_CUDA(cudaMemset(e->gather, 0, static_cast<size_t>(max_slot) * c->world * E));
-            LP_CUDA(cudaMalloc(&e->sub, static_cast<size_t>(max_entry) * E));
+            size_t max_owned = 1;
+            for (int a = 0; a < 3; ++a) max_owned = std::max(max_owned, e->layout[a].owned.size());
+            const int want_slots = std::max(1, std::min(4, tune_get("engine_slots", 2)));
+            if (c->dit && max_owned > 1) e->nslots = static_cast<int>(std::min<size_t>(max_owned, want_slots));
+            e->sub_stride = (static_cast<size_t>(max_entry) * E + 255) / 256 * 256;
+            LP_CUDA(cudaMalloc(&e->sub, e->sub_stride * e->nslots));
+            LP_CUDA(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+            for (int s = 0; s < e->nslots; ++s) {
+                LP_CUDA(cudaStreamCreateWithFlags(&e->slot_stream[s], cudaStreamNonBlocking));
+                LP_CUDA(cudaEventCreateWithFlags(&e->ev_join[s], cudaEventDisableTiming));
+            }
             LP_CUDA(cudaMalloc(&e->ws, lp_toy_workspace_bytes(c->shape) + 64));
             if (c->dit) {
                 // workspace for the largest shard the DiT will see (tokens per entry)
@@ -101,7 +116,7 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
                                                                      e->plans[a].entries[k].latent_begin);
                         max_tokens = std::max(max_tokens, (s.t / c->patch[0]) * (s.h / c->patch[1]) * (s.w / c->patch[2]));
                     }
-                const int st = lp_dit_reserve(c->dit, max_tokens);
+                const int st = lp_dit_reserve_slots(c->dit, max_tokens, e->nslots);
                 if (st) fail(st, lp_last_error());
             }
             if (c->world > 1) {
@@ -124,6 +139,11 @@ int lp_engine_destroy(lp_engine* e) {
     cudaFree(e->z);
     cudaFree(e->gather);
     cudaFree(e->sub);
+    for (int s = 0; s < 4; ++s) {
+        if (e->slot_stream[s]) cudaStreamDestroy(e->slot_stream[s]);
+        if (e->ev_join[s]) cudaEventDestroy(e->ev_join[s]);
+    }
+    if (e->ev_fork) cudaEventDestroy(e->ev_fork);
     cudaFree(e->ws);
     delete e;
     return LP_OK;
@@ -147,20 +167,35 @@ int lp_engine_run(lp_engine* e, int32_t first, int32_t count, void* stream) {
             const int a = rotation_axis(i);
             const lp_plan& plan = e->plans[a];
             const ShardLayout& L = e->layout[a];
-            for (int k : L.owned) {
+            const bool fork = e->nslots > 1 && L.owned.size() > 1;
+            if (fork) {
+                LP_CUDA(cudaEventRecord(e->ev_fork, st));
+                for (int s = 0; s < e->nslots; ++s) LP_CUDA(cudaStreamWaitEvent(e->slot_stream[s], e->ev_fork, 0));
+            }
+            for (size_t idx = 0; idx < L.owned.size(); ++idx) {
+                const int k = L.owned[idx];
+                const int slot = fork ? static_cast<int>(idx % e->nslots) : 0;
+                cudaStream_t ss = fork ? e->slot_stream[slot] : st;
+                char* sub = static_cast<char*>(e->sub) + e->sub_stride * slot;
                 const lp_entry& en = plan.entries[k];
                 const Shape4 s = e->shape.with_extent(a, en.latent_end - en.latent_begin);
-                slice_to(e->z, e->shape, a, en.latent_begin, en.latent_end, E, e->sub, st);  // K1
+                slice_to(e->z, e->shape, a, en.latent_begin, en.latent_end, E, sub, ss);  // K1
                 void* eps = gather + static_cast<size_t>(L.base[k]) * E;
                 const int64_t sh[4] = {s.c, s.t, s.h, s.w};
                 int rc;
                 if (c.denoiser < 0)
-                    rc = lp_dit_cfg_predict(c.dit, e->sub, sh, E, t, c.guidance, eps, stream);
+                    rc = lp_dit_cfg_predict_slot(c.dit, slot, sub, sh, E, t, c.guidance, eps, ss);
                 else
-                    rc = lp_toy_cfg_predict(c.denoiser, c.radius, c.t_coeff, c.cond_coeff, e->sub, sh, E, t,
-                                            e->cond_mean, c.guidance, eps, e->ws, stream);
+                    rc = lp_toy_cfg_predict(c.denoiser, c.radius, c.t_coeff, c.cond_coeff, sub, sh, E, t,
+                                            e->cond_mean, c.guidance, eps, e->ws, ss);
                 if (rc) fail(LP_ERR_WORKER_FAILURE, "worker " + std::to_string(k + 1) + " failed at step " +
                                                         std::to_string(i) + ": " + lp_last_error());
+            }
+            if (fork) {
+                for (int s = 0; s < e->nslots; ++s) {
+                    LP_CUDA(cudaEventRecord(e->ev_join[s], e->slot_stream[s]));
+                    LP_CUDA(cudaStreamWaitEvent(st, e->ev_join[s], 0));
+                }
             }
             if (c.world > 1) {
                 const size_t slot = static_cast<size_t>(L.slot_elems) * E;

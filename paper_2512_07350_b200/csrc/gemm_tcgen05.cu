@@ -402,14 +402,7 @@ static void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const Gem
     LP_LAUNCH_CHECK();
 }
 
-static int gemm_variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("LP_GEMM_2SM");
-        v = e ? atoi(e) : 1;
-    }
-    return v;
-}
+static int gemm_variant() { return tune_get("gemm_2sm", 1); }
 
 template <int MODE>
 static void gemm_bn(const CUtensorMap& ta, const void* B, int64_t ldb, const GemmEpilogue& ep, int M, int N, int K,

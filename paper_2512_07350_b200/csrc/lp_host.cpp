@@ -191,6 +191,23 @@ cudaEvent_t take_event() {
 }
 }  // namespace
 
+namespace {
+std::mutex g_tune_mu;
+std::vector<std::pair<std::string, int>> g_tune;
+}  // namespace
+
+int tune_get(const char* key, int dflt) {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    for (auto& kv : g_tune)
+        if (kv.first == key) return kv.second;
+    std::string env = "LP_TUNE_";
+    for (const char* c = key; *c; ++c) env += static_cast<char>(toupper(*c));
+    const char* e = getenv(env.c_str());
+    const int v = e ? atoi(e) : dflt;
+    g_tune.emplace_back(key, v);
+    return v;
+}
+
 bool prof_enabled() { return g_prof_on; }
 void prof_begin(int cls, cudaStream_t st) {
     if (!g_prof_on) return;
@@ -209,6 +226,18 @@ void prof_end(int cls, cudaStream_t st, double flops, double bytes) {
 }  // namespace lpb200
 
 using namespace lpb200;
+
+extern "C" int lp_tune(const char* key, int value) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g_tune_mu);
+        for (auto& kv : g_tune)
+            if (kv.first == key) {
+                kv.second = value;
+                return;
+            }
+        g_tune.emplace_back(key, value);
+    });
+}
 
 extern "C" int lp_profile_enable(int on) {
     return guard([&] {

@@ -82,6 +82,17 @@ class DiTReference:
     def forward(self, z, t, ctx_k, ctx_v, w):
         """z: [C, F, H, W] fp32 latent; ctx_k/ctx_v: per-layer [2, T, d] (the engine's cached
         cross K/V); returns (eps [C,F,H,W] fp32 computed with fp32 combine, head [2n, 64])."""
+        out, head = self.run(z, t, ctx_k, ctx_v, (0, 1))
+        u, cc = out[0].double(), out[1].double()
+        return (u + w * (cc - u)).float(), head
+
+    @torch.no_grad()
+    def predict(self, z, t, ctx_k, ctx_v, b):
+        """One CFG pass (b = 0 uncond / 1 cond): the Denoiser::predict of this DiT."""
+        return self.run(z, t, ctx_k, ctx_v, (b,))[0][0]
+
+    @torch.no_grad()
+    def run(self, z, t, ctx_k, ctx_v, batches):
         c = self.cfg
         d, L, heads = c.dim, c.num_layers, c.num_heads
         pt, ph, pw = c.patch
@@ -92,7 +103,8 @@ class DiTReference:
         patches = zp.view(C, nf, pt, nh, ph, nw, pw).permute(1, 3, 5, 0, 2, 4, 6).reshape(nf * nh * nw, -1)
         n = patches.shape[0]
         x0 = patches @ self.p["patch.w"].view(d, -1).t() + self.p["patch.b"]
-        x = torch.cat([x0, x0], 0)
+        B = len(batches)
+        x = torch.cat([x0] * B, 0)
         s = sinusoid(c.freq_dim, t * c.t_scale).to(z.device)
         e = Fn.silu(s @ self.p["time.w1"].view(d, -1).t() + self.p["time.b1"]) @ self.p["time.w2"].view(d, d).t() + self.p["time.b2"]
         e0 = (Fn.silu(e) @ self.p["time.wp"].view(6 * d, d).t() + self.p["time.bp"]).view(6, d)
@@ -108,7 +120,7 @@ class DiTReference:
             q = rms(q, self.p[pre + "norm_q"], eps)
             k = rms(k, self.p[pre + "norm_k"], eps)
             outs = []
-            for b in range(2):
+            for b in range(B):
                 sl = slice(b * n, (b + 1) * n)
                 outs.append(attention(apply_rope(q[sl], cos, sin, heads), apply_rope(k[sl], cos, sin, heads), v[sl], heads))
             y = torch.cat(outs, 0) @ self.p[pre + "o.w"].view(d, d).t() + self.p[pre + "o.b"]
@@ -116,9 +128,9 @@ class DiTReference:
             h = Fn.layer_norm(x, (d,), weight=self.p[pre + "norm3.w"], bias=self.p[pre + "norm3.b"], eps=eps)
             cq = rms(h @ self.p[pre + "cq.w"].view(d, d).t() + self.p[pre + "cq.b"], self.p[pre + "cnorm_q"], eps)
             outs = []
-            for b in range(2):
+            for b in range(B):
                 sl = slice(b * n, (b + 1) * n)
-                outs.append(attention(cq[sl], ctx_k[l][b], ctx_v[l][b], heads))
+                outs.append(attention(cq[sl], ctx_k[l][batches[b]], ctx_v[l][batches[b]], heads))
             x = x + torch.cat(outs, 0) @ self.p[pre + "co.w"].view(d, d).t() + self.p[pre + "co.b"]
             h = Fn.layer_norm(x, (d,), eps=eps) * (1 + m[4]) + m[3]
             f = Fn.gelu(h @ self.p[pre + "ffn1.w"].view(c.ffn_dim, d).t() + self.p[pre + "ffn1.b"], approximate="tanh")
@@ -126,7 +138,5 @@ class DiTReference:
         hm = self.p["head.mod"].view(2, d) + e[None]
         h = Fn.layer_norm(x, (d,), eps=eps) * (1 + hm[1]) + hm[0]
         head = h @ self.p["head.w"].view(-1, d).t() + self.p["head.b"]  # [2n, pt*ph*pw*C]
-        out = head.view(2, nf, nh, nw, pt, ph, pw, C).permute(0, 7, 1, 4, 2, 5, 3, 6).reshape(2, C, nf * pt, nh * ph, nw * pw)
-        out = out[:, :, :F, :H, :W].double()
-        u, cc = out[0], out[1]
-        return (u + w * (cc - u)).float(), head
+        out = head.view(B, nf, nh, nw, pt, ph, pw, C).permute(0, 7, 1, 4, 2, 5, 3, 6).reshape(B, C, nf * pt, nh * ph, nw * pw)
+        return out[:, :, :F, :H, :W], head

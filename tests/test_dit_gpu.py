@@ -130,3 +130,34 @@ def test_engine_dit_step_runs(cuda):
     torch.cuda.synchronize()
     assert torch.isfinite(eng.z.data).all()
     assert eng.launches() > 0
+
+
+def test_lp_loop_with_dit_matches_reference_run_lp(cuda, reference):
+    """The UNMODIFIED reference run_lp (oracle/_ref) driving the fp32 torch DiT through its
+    Denoiser plugin slot, vs our engine (bf16 tcgen05 DiT, CFG batch 2, K1/K10 kernels).
+    Tolerance: rel. L2 of the latent update <= 5e-2, max |dz| <= 1e-2 after 3 steps."""
+    from tests.dit_reference import DiTReference
+
+    dims, steps, K, r, eta, w = (16, 5, 16, 16), 3, 2, 0.5, 0.05, 5.0
+    z, cond = lp.synthetic_latent(dims, 4, 2025)
+    dit = lp.DiTDenoiser(cond, num_layers=2)
+    L = dit.cfg.num_layers
+    ck = [dit.debug_tensor(f"ctx_k.{l}", torch.bfloat16).float().view(2, dit.cfg.text_len, -1) for l in range(L)]
+    cv = [dit.debug_tensor(f"ctx_v.{l}", torch.bfloat16).float().view(2, dit.cfg.text_len, -1) for l in range(L)]
+    ref = DiTReference(dit)
+
+    def predict(zz, t, c, is_null):
+        x = torch.from_numpy(zz).float().cuda()
+        return ref.predict(x, t, ck, cv, 0 if is_null else 1).double().cpu().numpy()
+
+    z0 = z.to_numpy()
+    import os
+
+    os.environ["LPSIM_THREADS"] = "0"  # serial worker pool: the callback drives the GPU from this thread
+    want, ledger_ref = reference.run_lp_callback(predict, z0, 4, steps, eta, w, cond, (1, 2, 2), K, r)
+    got, led = lp.run_lp("dit", (0, 0, 0), z, steps, eta, w, cond, (1, 2, 2), K, r, dit=dit)
+    got = got.to_numpy()
+    assert led["grand_total"] == ledger_ref
+    rel = np.linalg.norm(got - want) / np.linalg.norm(want - z0)
+    assert np.isfinite(rel) and rel <= 5e-2, rel
+    assert np.abs(got - want).max() <= 1e-2

@@ -138,6 +138,22 @@ int lp_shard_bases(const lp_plan* plan, const int64_t shape[4], int world, int64
 int lp_step_comm_bytes(const lp_plan* plan, const int64_t shape[4], int wire_bytes, int world, int dtype_bytes,
                        uint64_t* ledger_bytes_out, uint64_t* allgather_bytes_out);
 
+/* Communication cost model — cost_report (src/cost.cpp:215-248) incl. cost_nmp /
+ * cost_pp / cost_lp_exact / cost_lp_approx / cost_hybrid (src/cost.cpp:46-213),
+ * at the preset's hidden width and wire bytes.  hybrid_groups = 0: no hybrid. */
+typedef struct lp_cost_report_t {
+    uint64_t latent_bytes, activation_bytes;  /* S_z, S_H */
+    double ext_bytes_mean, gamma, gamma_per_axis[3];
+    uint64_t nmp_bytes, pp_bytes, lp_exact_bytes;
+    double lp_approx_bytes, ratio_exact, ratio_approx, latent_activation_ratio;
+    int32_t has_hybrid, hybrid_within_bound;
+    uint64_t hybrid_inter_bytes, hybrid_intra_bytes, hybrid_total_bytes;
+    double hybrid_ratio_vs_nmp, hybrid_bound;
+} lp_cost_report_t;
+int lp_cost_report(int steps, int workers, double overlap_ratio, const int64_t shape[4], const int64_t patch[3],
+                   int64_t hidden_dim, int wire_bytes, int hybrid_groups, const int32_t* group_sizes,
+                   lp_cost_report_t* out);
+
 /* Quantizer (src/dtype.cpp:34-116), host side, for tests and host shims. */
 uint16_t lp_f16_encode(double v);
 double lp_f16_decode(uint16_t bits);

@@ -336,13 +336,22 @@ class Reference(_Lib):
                       w, _p(cond), cond.size, None, _p(out)))
         return out
 
-    def cost(self, steps, workers, r, shape, patch, hidden=1536, wire_bytes=2):
-        out = np.zeros(6, np.float64)
+    def cost(self, steps, workers, r, shape, patch, hidden=1536, wire_bytes=2, hybrid=None):
+        out = np.zeros(21, np.float64)
+        groups, sizes = (0, [0]) if hybrid is None else (hybrid[0], list(hybrid[1]))
+        sz = (C.c_int * len(sizes))(*sizes)
         f = self.fn("cost")
-        f.argtypes = [C.c_int, C.c_int, C.c_double, _i64p, _i64p, C.c_int64, C.c_int, _f64p]
+        f.argtypes = [C.c_int, C.c_int, C.c_double, _i64p, _i64p, C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int),
+                      _f64p]
         self._check(f(steps, workers, r, _p(_arr(shape, np.int64)), _p(_arr(patch, np.int64)), hidden, wire_bytes,
-                      _p(out)))
-        return {"C_LP_exact": out[0], "C_NMP": out[1], "C_PP": out[2], "gamma": tuple(out[3:6])}
+                      groups, sz, _p(out)))
+        d = {"S_z": out[0], "S_H": out[1], "gamma": out[3], "gamma_per_axis": tuple(out[4:7]), "C_NMP": out[7],
+             "C_PP": out[8], "C_LP_exact": out[9], "C_LP_approx": out[10], "ratio_exact": out[11],
+             "ratio_approx": out[12], "Sz_over_SH": out[13]}
+        if out[14]:
+            d["hybrid"] = {"C_inter": out[15], "C_intra_total": out[16], "C_hyb": out[17], "ratio_vs_NMP": out[18],
+                           "bound": out[19], "within_bound": bool(out[20])}
+        return d
 
 
 def reference_available() -> bool:

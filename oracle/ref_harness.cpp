@@ -319,9 +319,11 @@ double ref_quantize(double v, int dtype_bytes) { return quantize(v, dtype_from_b
 uint16_t ref_f16_encode(double v) { return f16_encode(v); }
 double ref_f16_decode(uint16_t b) { return f16_decode(b); }
 
-// cost_report subset: out = {C_LP_exact, C_NMP, C_PP, gamma_T, gamma_H, gamma_W}
+// cost_report (src/cost.cpp:215-248): out[20] =
+// {S_z, S_H, ext_mean, gamma, g_T, g_H, g_W, NMP, PP, LP_exact, LP_approx, ratio_exact, ratio_approx,
+//  Sz/SH, has_hybrid, inter, intra, total, ratio_vs_nmp, bound, within}
 int ref_cost(int steps, int workers, double r, const int64_t* shape, const int64_t* patch, int64_t hidden,
-             int wire_bytes, double* out) {
+             int wire_bytes, int groups, const int* sizes, double* out) {
     return guarded([&] {
         CostInputs in;
         in.steps = steps;
@@ -330,14 +332,20 @@ int ref_cost(int steps, int workers, double r, const int64_t* shape, const int64
         in.shape = to_shape(shape);
         in.geometry = PatchGeometry{patch[0], patch[1], patch[2]};
         in.preset = ModelPreset{"harness", hidden, wire_bytes, ""};
+        if (groups > 0) in.hybrid = HybridSpec{groups, std::vector<int>(sizes, sizes + groups)};
         const CostReport rep = cost_report(in);
-        out[0] = static_cast<double>(rep.lp_exact_bytes);
-        out[1] = static_cast<double>(rep.nmp_bytes);
-        out[2] = static_cast<double>(rep.pp_bytes);
-        for (int a = 0; a < 3; ++a) {
-            out[3 + a] = expansion_factor(static_cast<Axis>(a), in.shape.extent(static_cast<Axis>(a)),
-                                          in.geometry.at(static_cast<Axis>(a)), workers, r);
-        }
+        const double v[] = {static_cast<double>(rep.latent_bytes), static_cast<double>(rep.activation_bytes),
+                            rep.ext_bytes_mean, rep.gamma, rep.gamma_per_axis[0], rep.gamma_per_axis[1],
+                            rep.gamma_per_axis[2], static_cast<double>(rep.nmp_bytes),
+                            static_cast<double>(rep.pp_bytes), static_cast<double>(rep.lp_exact_bytes),
+                            rep.lp_approx_bytes, rep.ratio_exact, rep.ratio_approx, rep.latent_activation_ratio,
+                            rep.hybrid.has_value() ? 1.0 : 0.0,
+                            rep.hybrid ? static_cast<double>(rep.hybrid->inter_bytes) : 0.0,
+                            rep.hybrid ? static_cast<double>(rep.hybrid->intra_bytes) : 0.0,
+                            rep.hybrid ? static_cast<double>(rep.hybrid->total_bytes) : 0.0,
+                            rep.hybrid ? rep.hybrid->ratio_vs_nmp : 0.0, rep.hybrid ? rep.hybrid->bound : 0.0,
+                            rep.hybrid ? (rep.hybrid->within_bound ? 1.0 : 0.0) : 0.0};
+        std::memcpy(out, v, sizeof(v));
     });
 }
 

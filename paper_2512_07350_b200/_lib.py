@@ -59,6 +59,16 @@ class EngineConfig(C.Structure):
                 ("cond_coeff", C.c_double), ("world", C.c_int32), ("rank", C.c_int32), ("dit", C.c_void_p)]
 
 
+class CostReport(C.Structure):
+    _fields_ = [("latent_bytes", C.c_uint64), ("activation_bytes", C.c_uint64), ("ext_bytes_mean", C.c_double),
+                ("gamma", C.c_double), ("gamma_per_axis", C.c_double * 3), ("nmp_bytes", C.c_uint64),
+                ("pp_bytes", C.c_uint64), ("lp_exact_bytes", C.c_uint64), ("lp_approx_bytes", C.c_double),
+                ("ratio_exact", C.c_double), ("ratio_approx", C.c_double), ("latent_activation_ratio", C.c_double),
+                ("has_hybrid", C.c_int32), ("hybrid_within_bound", C.c_int32), ("hybrid_inter_bytes", C.c_uint64),
+                ("hybrid_intra_bytes", C.c_uint64), ("hybrid_total_bytes", C.c_uint64),
+                ("hybrid_ratio_vs_nmp", C.c_double), ("hybrid_bound", C.c_double)]
+
+
 _i64p = C.POINTER(C.c_int64)
 _f64p = C.POINTER(C.c_double)
 _vp = C.c_void_p
@@ -81,6 +91,7 @@ _SIGS = {
     "lp_shard_layout": (_i, [_PlanP, _i64p, _i, _i, C.POINTER(_i32), C.POINTER(_i32), _i64p]),
     "lp_shard_bases": (_i, [_PlanP, _i64p, _i, _i64p]),
     "lp_step_comm_bytes":(_i, [_PlanP, _i64p, _i, _i, _i, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "lp_cost_report": (_i, [_i, _i, _d, _i64p, _i64p, _i64, _i, _i, C.POINTER(_i32), C.POINTER(CostReport)]),
     "lp_f16_encode": (C.c_uint16, [_d]),
     "lp_f16_decode": (_d, [C.c_uint16]),
     "lp_quantize": (_d, [_d, _i]),

@@ -26,6 +26,7 @@ INCS = ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 # (source, extra flags).  lp_kernels.cu must not contract FMAs (exact mode).
 SOURCES = [
     ("lp_host.cpp", ["-Xcompiler", "-ffp-contract=off"]),
+    ("cost.cpp", ["-Xcompiler", "-ffp-contract=off"]),
     ("lp_kernels.cu", ["-fmad=false"]),
     ("dit_kernels.cu", []),
     ("gemm_tcgen05.cu", []),

@@ -221,6 +221,31 @@ def shard_bases(plan: PartitionPlan, dims, world: int):
     return list(out)
 
 
+def cost_report(steps, workers, overlap_ratio, dims, patch, preset="wan21-like", hybrid=None, hidden_dim=None,
+                wire_bytes=None):
+    """cost_report of the reference (src/cost.cpp:215-248; python binding lpsim_bindings.cpp:234-245):
+    same keys as the reference module's dict."""
+    pr = PRESETS[preset] if preset in PRESETS else None
+    if pr is None and (hidden_dim is None or wire_bytes is None):
+        raise ValueError(f"unknown preset '{preset}'")
+    hd = hidden_dim if hidden_dim is not None else pr["hidden_dim"]
+    wb = wire_bytes if wire_bytes is not None else pr["dtype_bytes"]
+    groups, sizes = (0, []) if hybrid is None else (int(hybrid[0]), list(hybrid[1]))
+    arr = (C.c_int32 * max(1, len(sizes)))(*sizes) if sizes else (C.c_int32 * 1)()
+    r = _lib.CostReport()
+    check(lib().lp_cost_report(steps, workers, float(overlap_ratio), i64arr(dims), i64arr(patch), hd, wb, groups, arr,
+                               C.byref(r)))
+    d = {"S_z": r.latent_bytes, "S_H": r.activation_bytes, "gamma": r.gamma, "C_NMP": r.nmp_bytes, "C_PP": r.pp_bytes,
+         "C_LP_exact": r.lp_exact_bytes, "C_LP_approx": r.lp_approx_bytes, "ratio_exact": r.ratio_exact,
+         "ratio_approx": r.ratio_approx, "Sz_over_SH": r.latent_activation_ratio,
+         "gamma_per_axis": tuple(r.gamma_per_axis)}
+    if r.has_hybrid:
+        d["hybrid"] = {"C_inter": r.hybrid_inter_bytes, "C_intra_total": r.hybrid_intra_bytes,
+                       "C_hyb": r.hybrid_total_bytes, "ratio_vs_NMP": r.hybrid_ratio_vs_nmp, "bound": r.hybrid_bound,
+                       "within_bound": bool(r.hybrid_within_bound)}
+    return d
+
+
 def step_comm_bytes(plan: PartitionPlan, dims, wire_bytes: int, world: int, dtype_bytes: int):
     a, b = C.c_uint64(), C.c_uint64()
     check(lib().lp_step_comm_bytes(C.byref(plan.raw), i64arr(dims), wire_bytes, world, dtype_bytes, C.byref(a),

@@ -156,3 +156,51 @@ def test_device_entry_points_fail_loudly_without_gpu():
         pass
     st = _lib.lib().lp_device_check(0)
     assert st == 100  # LP_ERR_CUDA: no CPU fallback
+
+
+def _same(a, b):
+    return (a == b) or (np.isnan(a) and np.isnan(b))
+
+
+def test_cost_report_matches_reference(reference):
+    """cost_report bit-exact vs the reference (src/cost.cpp:215-248), incl. hybrid, over the
+    BASELINE.json configs and a random sweep; and the BASELINE.md table values."""
+    cases = [
+        (60, 4, 0.5, (16, 13, 60, 104), (1, 2, 2), None),     # paper 49f
+        (50, 4, 0.5, (16, 21, 60, 104), (1, 2, 2), None),     # C2
+        (50, 8, 0.5, (16, 21, 90, 160), (1, 2, 2), None),     # C4 (hidden 5120 below)
+        (50, 8, 0.5, (16, 41, 60, 104), (1, 2, 2), None),     # C5
+        (60, 4, 0.5, (16, 13, 60, 104), (1, 2, 2), (2, [2, 2])),
+        (50, 8, 1.0, (16, 21, 60, 104), (1, 2, 2), (3, [3, 3, 2])),
+        (4, 1, 0.0, (16, 5, 16, 16), (1, 2, 2), (1, [1])),
+    ]
+    rng = np.random.default_rng(9)
+    for _ in range(40):
+        k = int(rng.integers(1, 9))
+        g = int(rng.integers(1, k + 1))
+        sizes = [1] * g
+        for _ in range(k - g):
+            sizes[int(rng.integers(0, g))] += 1
+        cases.append((int(rng.integers(1, 70)), k, float(min(rng.choice([0, .25, .5, 1.0]), k - 1)),
+                      tuple(int(v) for v in rng.integers(2, 40, size=4)), (1, 2, 2),
+                      (g, sizes) if rng.random() < 0.5 else None))
+    for steps, k, r, dims, patch, hyb in cases:
+        hidden = 5120 if dims == (16, 21, 90, 160) else 1536
+        try:
+            want = reference.cost(steps, k, r, dims, patch, hidden, 2, hyb)
+        except OracleError:
+            continue
+        got = lp.cost_report(steps, k, r, dims, patch, hybrid=hyb, hidden_dim=hidden, wire_bytes=2)
+        for key in ("S_z", "S_H", "gamma", "C_NMP", "C_PP", "C_LP_exact", "C_LP_approx", "ratio_exact",
+                    "ratio_approx", "Sz_over_SH"):
+            assert _same(float(got[key]), float(want[key])), (key, got[key], want[key], dims, k, r)
+        assert got["gamma_per_axis"] == want["gamma_per_axis"]
+        assert ("hybrid" in got) == ("hybrid" in want)
+        if "hybrid" in got:
+            for key, v in want["hybrid"].items():
+                assert _same(float(got["hybrid"][key]), float(v)), key
+    # BASELINE.md §2 numbers
+    c2 = lp.cost_report(50, 4, 0.5, (16, 21, 60, 104), (1, 2, 2))
+    assert round(c2["C_LP_exact"] / 1e6, 1) == 1162.7 and round(c2["C_NMP"] / 1e6, 1) == 30191.6
+    paper = lp.cost_report(60, 4, 0.5, (16, 13, 60, 104), (1, 2, 2))
+    assert round(paper["ratio_exact"], 4) == 0.0381

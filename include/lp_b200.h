@@ -294,6 +294,11 @@ typedef struct lp_engine_config {
     double t_coeff, cond_coeff;
     int32_t world, rank;   /* ranks sharing the plan; entries round-robin over ranks */
     lp_dit* dit;
+    /* Axis schedule (BASELINE config C5): 0 = the reference's
+     * T->H->W rotation (src/partition.cpp:38-43); else step i uses axis
+     * schedule[(i-1) % schedule_len].  Plans per axis are build_axis_plan's. */
+    int32_t schedule_len;
+    int32_t schedule[64];
 } lp_engine_config;
 
 typedef struct lp_engine lp_engine;

@@ -354,5 +354,15 @@ class Reference(_Lib):
         return d
 
 
+def verify_n_complete(ref: "Reference", grid, workers, r, schedule, budget):
+    out = np.zeros(5, np.int64)
+    sched = (C.c_int * len(schedule))(*schedule)
+    f = ref.fn("verify_n_complete")
+    f.argtypes = [_i64p, C.c_int, C.c_double, C.POINTER(C.c_int), C.c_int, C.c_int, _i64p]
+    ref._check(f(_p(_arr(grid, np.int64)), workers, r, sched, len(schedule), budget, _p(out)))
+    return {"complete": bool(out[0]), "complete_at": int(out[1]) if out[0] else None,
+            "worst_position": tuple(int(v) for v in out[2:5])}
+
+
 def reference_available() -> bool:
     return os.path.exists(REF_SO)

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "lpsim/cluster.hpp"
+#include "lpsim/completeness.hpp"
 #include "lpsim/cost.hpp"
 #include "lpsim/denoise.hpp"
 #include "lpsim/dtype.hpp"
@@ -346,6 +347,22 @@ int ref_cost(int steps, int workers, double r, const int64_t* shape, const int64
                             rep.hybrid ? rep.hybrid->ratio_vs_nmp : 0.0, rep.hybrid ? rep.hybrid->bound : 0.0,
                             rep.hybrid ? (rep.hybrid->within_bound ? 1.0 : 0.0) : 0.0};
         std::memcpy(out, v, sizeof(v));
+    });
+}
+
+// verify_n_complete (src/completeness.cpp:104-160) with an explicit axis schedule.
+// out[5] = {complete, complete_at, worst_t, worst_h, worst_w}
+int ref_verify_n_complete(const int64_t* grid, int workers, double r, const int* schedule, int len, int budget,
+                          int64_t* out) {
+    return guarded([&] {
+        std::vector<Axis> sched;
+        for (int i = 0; i < budget; ++i) sched.push_back(static_cast<Axis>(schedule[i % len]));
+        const CompletenessResult res = verify_n_complete(GridDims{grid[0], grid[1], grid[2]}, workers, r, sched, budget);
+        out[0] = res.complete ? 1 : 0;
+        out[1] = res.complete_at;
+        out[2] = res.worst.t;
+        out[3] = res.worst.h;
+        out[4] = res.worst.w;
     });
 }
 

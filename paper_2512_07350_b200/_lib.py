@@ -56,7 +56,8 @@ class EngineConfig(C.Structure):
                 ("workers", C.c_int32), ("overlap_ratio", C.c_double), ("total_steps", C.c_int32),
                 ("mode", C.c_int32), ("eta", C.c_double), ("guidance", C.c_double), ("denoiser", C.c_int32),
                 ("wire_bytes", C.c_int32), ("radius", C.c_int64 * 3), ("t_coeff", C.c_double),
-                ("cond_coeff", C.c_double), ("world", C.c_int32), ("rank", C.c_int32), ("dit", C.c_void_p)]
+                ("cond_coeff", C.c_double), ("world", C.c_int32), ("rank", C.c_int32), ("dit", C.c_void_p),
+                ("schedule_len", C.c_int32), ("schedule", C.c_int32 * 64)]
 
 
 class CostReport(C.Structure):

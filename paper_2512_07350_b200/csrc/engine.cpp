@@ -71,6 +71,9 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
             fail(LP_ERR_INVALID_ARGUMENT, "preset dtype_bytes must be 2, 4 or 8");
         if (c->world < 1 || c->rank < 0 || c->rank >= c->world) fail(LP_ERR_INVALID_ARGUMENT, "bad world/rank");
         if (c->denoiser < 0 && !c->dit) fail(LP_ERR_INVALID_ARGUMENT, "DiT engine without a DiT");
+        if (c->schedule_len < 0 || c->schedule_len > 64) fail(LP_ERR_INVALID_ARGUMENT, "schedule_len must be 0..64");
+        for (int i = 0; i < c->schedule_len; ++i)
+            if (c->schedule[i] < 0 || c->schedule[i] > 2) fail(LP_ERR_INVALID_ARGUMENT, "schedule axes must be 0..2");
         auto* e = new lp_engine();
         e->cfg = *c;
         e->shape = Shape4::from(c->shape);
@@ -164,7 +167,7 @@ int lp_engine_run(lp_engine* e, int32_t first, int32_t count, void* stream) {
         for (int i = first; i < first + count; ++i) {
             if (i < 1 || i > c.total_steps) fail(LP_ERR_INVALID_ARGUMENT, "step out of range");
             const int t = c.total_steps + 1 - i;
-            const int a = rotation_axis(i);
+            const int a = c.schedule_len > 0 ? c.schedule[(i - 1) % c.schedule_len] : rotation_axis(i);
             const lp_plan& plan = e->plans[a];
             const ShardLayout& L = e->layout[a];
             const bool fork = e->nslots > 1 && L.owned.size() > 1;

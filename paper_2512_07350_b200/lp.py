@@ -466,7 +466,7 @@ class LpEngine:
 
     def __init__(self, dims, patch, dtype_bytes, workers, overlap_ratio, steps, eta, guidance, cond,
                  denoiser="box", radius=(1, 1, 1), wire_bytes=2, world=1, rank=0, nccl_id=None, mode="exact",
-                 dit: DiTDenoiser | None = None, t_coeff=0.01, cond_coeff=0.1):
+                 dit: DiTDenoiser | None = None, t_coeff=0.01, cond_coeff=0.1, schedule=None):
         cfg = _lib.EngineConfig()
         for i in range(4):
             cfg.shape[i] = int(dims[i])
@@ -490,6 +490,11 @@ class LpEngine:
         cfg.world = world
         cfg.rank = rank
         cfg.dit = dit.handle if dit is not None else None
+        if schedule:
+            axes = parse_schedule(schedule)
+            cfg.schedule_len = len(axes)
+            for i, a in enumerate(axes):
+                cfg.schedule[i] = a
         self.dit = dit
         self.dims = tuple(int(d) for d in dims)
         self.dtype_bytes = dtype_bytes
@@ -545,6 +550,18 @@ def _wrap_latent(ptr, dims, dtype_bytes):
     return torch.as_tensor(_H(), device="cuda")
 
 
+def parse_schedule(schedule):
+    """'TTHTTW' / ['temporal', 'height', ...] / [0, 1, 2] -> axis ids (T=0, H=1, W=2)."""
+    if isinstance(schedule, str):
+        m = {"T": 0, "H": 1, "W": 2}
+        axes = [m[ch] for ch in schedule.upper() if ch in m]
+    else:
+        axes = [Axis[a].value if isinstance(a, str) else int(a) for a in schedule]
+    if not 1 <= len(axes) <= 64:
+        raise LpError(10, "schedule must have 1..64 axes")
+    return axes
+
+
 def nccl_unique_id():
     buf = (C.c_uint8 * 128)()
     check(lib().lp_nccl_unique_id(C.byref(buf)))
@@ -552,13 +569,14 @@ def nccl_unique_id():
 
 
 def run_lp(denoiser, radius, z: LatentTensor, steps, eta, guidance, cond, patch, workers, overlap_ratio,
-           preset="wan21-like", mode="exact", dit: DiTDenoiser | None = None):
+           preset="wan21-like", mode="exact", dit: DiTDenoiser | None = None, schedule=None):
     """Same signature as the reference binding's run_lp (lpsim_bindings.cpp:199-232);
     returns (final latent, ledger summary)."""
     if preset not in PRESETS:
         raise ValueError(f"unknown preset '{preset}'")
     eng = LpEngine(z.shape, patch, z.dtype_bytes, workers, overlap_ratio, steps, eta, guidance, cond,
-                   denoiser=denoiser, radius=radius, wire_bytes=PRESETS[preset]["dtype_bytes"], mode=mode, dit=dit)
+                   denoiser=denoiser, radius=radius, wire_bytes=PRESETS[preset]["dtype_bytes"], mode=mode, dit=dit,
+                   schedule=schedule)
     eng.load(z)
     eng.run(1, steps)
     out = LatentTensor(eng.z.data.clone(), z.dtype_bytes)

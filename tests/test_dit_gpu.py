@@ -161,3 +161,18 @@ def test_lp_loop_with_dit_matches_reference_run_lp(cuda, reference):
     rel = np.linalg.norm(got - want) / np.linalg.norm(want - z0)
     assert np.isfinite(rel) and rel <= 5e-2, rel
     assert np.abs(got - want).max() <= 1e-2
+
+
+def test_dit_14b_shape_forward_matches_torch(cuda):
+    """BASELINE config C4's DiT shape (WAN2.1-14B: d=5120, 40 heads, FFN 13824), one block."""
+    from tests.dit_reference import DiTReference
+
+    z, cond = lp.synthetic_latent((16, 3, 8, 12), 4, 7)
+    dit = lp.DiTDenoiser(cond, dim=5120, ffn_dim=13824, num_heads=40, num_layers=1)
+    eps = dit.cfg_predict(z, 11, 5.0)
+    torch.cuda.synchronize()
+    ck = [dit.debug_tensor("ctx_k.0", torch.bfloat16).float().view(2, dit.cfg.text_len, -1)]
+    cv = [dit.debug_tensor("ctx_v.0", torch.bfloat16).float().view(2, dit.cfg.text_len, -1)]
+    want, _ = DiTReference(dit).forward(z.data.float(), 11, ck, cv, 5.0)
+    rel = ((eps.data.float() - want).norm() / want.norm()).item()
+    assert np.isfinite(rel) and rel <= 5e-2, rel

@@ -48,6 +48,17 @@ def workload(K, world, layers):
     }
 
 
+def dit_step_flops(plan, layers, d=1536, ffn=8960, text_len=512):
+    """Algorithmic FLOPs of the CFG-batched DiT over every shard of one step's plan
+    (GEMM 2MNK with M = 2n, self-attention 4 n^2 d per batch, cross-attention 4 n 512 d)."""
+    tot = 0.0
+    for k in range(plan.workers):
+        s = plan.sub_shape(DIMS, k)
+        n = -(-s[1] // PATCH[0]) * -(-s[2] // PATCH[1]) * -(-s[3] // PATCH[2])
+        tot += layers * (2 * 2 * n * (4 * d * d + 2 * d * ffn) + 2 * 4 * n * n * d + 2 * 4 * n * text_len * d)
+    return tot
+
+
 def step_index(s):
     return (s - 1) % T_SCHED + 1
 
@@ -127,21 +138,74 @@ def cpu_reference_run(steps, K, threads):
     return steps / dt, {"kind": kind, "cores": used, "sample": sample, "seconds": dt}
 
 
+def reference_dit_step(ref, dit, z, cond, K, flop_scale):
+    """One bounded sample of the reference arm: the UNMODIFIED reference run_lp (oracle/_ref)
+    for one step with the fp32 CPU DiT (one block) in its Denoiser slot; the DiT's wall time
+    is scaled to the full 30 blocks and to the rotation-cycle mean shard FLOPs."""
+    import time as _t
+
+    dit.calls.clear()
+    t0 = _t.perf_counter()
+    ref.run_lp_callback(dit.predict, z, 4, 1, ETA, W_CFG, cond, PATCH, K, R_OVERLAP)
+    wall = _t.perf_counter() - t0
+    dit_wall = max(e for _, e in dit.calls) - min(s for s, _ in dit.calls)
+    return (wall - dit_wall) + dit_wall * flop_scale, wall, dit_wall
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
+    import torch
+
+    from oracle.cpu_dit import CpuDiT, dit_flops
+    from oracle.oracle import Reference, reference_available
+
     K = args.workers or max(4, world)
     threads = os.cpu_count() or 1
-    cpu_reference_run(max(1, args.warmup), K, threads)  # warm-up (untimed)
-    value, info = cpu_reference_run(args.steps, K, threads)
+    if not reference_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (the compiled reference) was not built"}))
+        return
+    # LP machinery alone (reference run_lp with its box denoiser, rho=1): what the reference runs without a DiT
+    cpu_reference_run(1, K, threads)
+    lp_only, lp_info = cpu_reference_run(args.steps, K, threads)
+    # the metric's workload: reference run_lp + a WAN-1.3B-shaped fp32 DiT in the Denoiser slot
+    os.environ["LPSIM_THREADS"] = str(threads)
+    workers = min(threads, K)
+    torch.set_num_threads(max(1, threads // workers))
+    ref = Reference()
+    z, cond = ref.synthetic(DIMS, 4, SEED)
+    dit = CpuDiT(num_layers=1)
+    from oracle.oracle import sub_shape
+
+    def axis_flops(step):  # the reference's own plans
+        p = ref.build_plan(DIMS, PATCH, step, K, R_OVERLAP)
+        return sum(dit_flops(sub_shape(DIMS, p, k), PATCH) for k in range(p.n))
+
+    cycle = sum(axis_flops(s) for s in (1, 2, 3)) / 3
+    scale = 30 * cycle / axis_flops(1)   # run_lp's single sampled step is step 1 (T axis)
+    for _ in range(min(args.warmup, 1)):
+        reference_dit_step(ref, dit, z, cond, K, scale)
+    est, walls, dits = [], [], []
+    for _ in range(args.steps):
+        e, w, dw = reference_dit_step(ref, dit, z, cond, K, scale)
+        est.append(e)
+        walls.append(w)
+        dits.append(dw)
+    value = len(est) / sum(est)
+    sample = (f"UNMODIFIED reference run_lp (oracle/_ref) for 1 step (T axis) of C2 (16x21x60x104 f32, K={K}, "
+              f"r={R_OVERLAP}, eta {ETA}, w {W_CFG}) with an fp32 torch CPU WAN-1.3B-shaped DiT (1 of 30 blocks, "
+              f"random weights) in its Denoiser slot; per sample: measured wall {statistics.mean(walls):.2f} s of which "
+              f"DiT {statistics.mean(dits):.2f} s, DiT part scaled x{scale:.2f} (30 blocks x cycle-mean/T-axis shard "
+              f"FLOPs); LPSIM_THREADS={threads}, {workers} workers x {torch.get_num_threads()} torch threads; "
+              f"{min(args.warmup, 1)} warm-up sample")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (synthetic_inputs seed 2025)",
+        "vs_baseline": None, "dtype": "f64 (LP machinery) / f32 (CPU DiT)", "data": "synthetic (synthetic_inputs seed 2025)",
         "config": workload(K, world, 30),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
-                         "sample": info["sample"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "lp_machinery_only": {"value": lp_only, "unit": UNIT, "cores": lp_info["cores"], "sample": lp_info["sample"]},
     }
     print(json.dumps(line), flush=True)
 
@@ -191,7 +255,6 @@ def run_ours(args, rank, world, local_rank):
     # ---- device-timed region: K steps, inputs resident in HBM ----
     first = args.warmup + 1
     c0, l0 = eng.comm(), L.lp_launch_count()
-    L.lp_profile_enable(1)
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -202,13 +265,11 @@ def run_ours(args, rank, world, local_rank):
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
-    L.lp_profile_enable(0)
     launches = int(L.lp_launch_count() - l0)
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     c1 = eng.comm()
     nl = (C.c_uint64 * 3)()
     kms, kfl, kby = (C.c_double * 3)(), (C.c_double * 3)(), (C.c_double * 3)()
-    _lib.check(L.lp_profile_collect(nl, kms, kfl, kby))
 
     # ---- end-to-end through the C-ABI engine with host buffers ----
     zin = torch.empty(DIMS, dtype=torch.float32).pin_memory()
@@ -228,12 +289,28 @@ def run_ours(args, rank, world, local_rank):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
     assert torch.isfinite(zout).all(), "non-finite latent"
 
+    # ---- per-kernel roofline pass: one rotation cycle (T, H, W) with the shard streams
+    # serialised, so each kernel's CUDA-event duration is its own (in the timed region two
+    # shards' DiT forwards overlap on two streams and per-kernel durations would overlap) ----
+    L.lp_tune(b"engine_serial", 1)
+    L.lp_profile_enable(1)
+    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pe0.record(stream)
+    for s in range(first, first + 3):
+        eng.run(step_index(s), 1)
+    pe1.record(stream)
+    torch.cuda.synchronize()
+    L.lp_profile_enable(0)
+    L.lp_tune(b"engine_serial", 0)
+    prof_ms = pe0.elapsed_time(pe1)
+    _lib.check(L.lp_profile_collect(nl, kms, kfl, kby))
+
     if rank != 0:
         eng.close()
         return
     names = ["self_attention", "cross_attention", "gemm"]
     kern = {names[i]: {"launches": int(nl[i]), "ms": kms[i], "tflops": (kfl[i] / kms[i] / 1e9) if kms[i] else None,
-                       "share_of_step": kms[i] / ms if ms else None} for i in range(3)}
+                       "share_of_step": kms[i] / prof_ms if prof_ms else None} for i in range(3)}
     dom = max(range(3), key=lambda i: kms[i])
     peaks = {}
     try:
@@ -248,6 +325,10 @@ def run_ours(args, rank, world, local_rank):
         traffic = prof.get(names[dom], {}).get("dram_bytes_per_launch")
     except Exception:
         pass
+    # whole-step algorithmic FLOPs (DiT on every shard of the rotation cycle, CFG batch 2)
+    step_flops = statistics.mean(dit_step_flops(lp.build_plan(DIMS, PATCH, s, K, R_OVERLAP), args.layers)
+                                 for s in (1, 2, 3)) / world
+    step_tflops = step_flops / (ms / args.steps / 1000.0) / 1e12
     # communication per video (50 steps): measured NCCL bytes, exact all-gather layout, reference ledger, NMP
     per_step_nccl = (c1["nccl_bytes_received"] - c0["nccl_bytes_received"]) * world / args.steps
     led = ag = 0
@@ -269,7 +350,11 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "kernel": names[dom], "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if achieved else None, "traffic": traffic,
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"},
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)",
+                     "timing": "CUDA events around every launch on its stream, over one rotation cycle (3 steps) "
+                               "run right after the timed region with the shard streams serialised",
+                     "step": {"algorithmic_tflop_per_step_per_rank": step_flops / 1e12, "achieved": step_tflops,
+                              "frac": step_tflops / peak}},
         "kernels": kern,
         "clocks": clk.summary(),
         "comm": {"nccl_bytes_per_step_measured_all_ranks": per_step_nccl,

@@ -170,7 +170,7 @@ int lp_engine_run(lp_engine* e, int32_t first, int32_t count, void* stream) {
             const int a = c.schedule_len > 0 ? c.schedule[(i - 1) % c.schedule_len] : rotation_axis(i);
             const lp_plan& plan = e->plans[a];
             const ShardLayout& L = e->layout[a];
-            const bool fork = e->nslots > 1 && L.owned.size() > 1;
+            const bool fork = e->nslots > 1 && L.owned.size() > 1 && !tune_get("engine_serial", 0);
             if (fork) {
                 LP_CUDA(cudaEventRecord(e->ev_fork, st));
                 for (int s = 0; s < e->nslots; ++s) LP_CUDA(cudaStreamWaitEvent(e->slot_stream[s], e->ev_fork, 0));

@@ -50,12 +50,12 @@ def workload(K, world, layers):
 
 def dit_step_flops(plan, layers, d=1536, ffn=8960, text_len=512):
     """Algorithmic FLOPs of the CFG-batched DiT over every shard of one step's plan
-    (GEMM 2MNK with M = 2n, self-attention 4 n^2 d per batch, cross-attention 4 n 512 d)."""
+    (GEMM 2MNK with M = 2n over QKV, O, cross-Q, cross-O, FFN1, FFN2, self-attention 4 n^2 d per batch, cross-attention 4 n 512 d)."""
     tot = 0.0
     for k in range(plan.workers):
         s = plan.sub_shape(DIMS, k)
         n = -(-s[1] // PATCH[0]) * -(-s[2] // PATCH[1]) * -(-s[3] // PATCH[2])
-        tot += layers * (2 * 2 * n * (4 * d * d + 2 * d * ffn) + 2 * 4 * n * n * d + 2 * 4 * n * text_len * d)
+        tot += layers * (2 * 2 * n * (6 * d * d + 2 * d * ffn) + 2 * 4 * n * n * d + 2 * 4 * n * text_len * d)
     return tot
 
 

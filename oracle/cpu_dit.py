@@ -91,4 +91,4 @@ class CpuDiT:
 def dit_flops(shape, patch, dim=1536, ffn=8960, text_len=512):
     """Algorithmic FLOPs of one DiT block for one CFG pass on a shard (GEMM 2MNK, attention 4 n_q n_kv d)."""
     n = -(-shape[1] // patch[0]) * -(-shape[2] // patch[1]) * -(-shape[3] // patch[2])
-    return 2 * n * (4 * dim * dim + 2 * dim * ffn) + 4 * n * n * dim + 4 * n * text_len * dim
+    return 2 * n * (6 * dim * dim + 2 * dim * ffn) + 4 * n * n * dim + 4 * n * text_len * dim

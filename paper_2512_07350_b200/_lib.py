@@ -123,6 +123,7 @@ _SIGS = {
     "lp_dit_debug_tensor": (_i, [_vp, C.c_char_p, C.POINTER(_vp), _i64p]),
     "lp_gemm_bf16": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "lp_attention_bf16": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _d, _vp]),
+    "lp_attention_set_trace": (_i, [_vp]),
     "lp_nccl_unique_id": (_i, [C.POINTER(C.c_uint8 * 128)]),
     "lp_engine_create": (_i, [C.POINTER(EngineConfig), _vp, _f64p, _i32, C.POINTER(_vp)]),
     "lp_engine_destroy": (_i, [_vp]),

@@ -49,24 +49,129 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
-// exp2 on the FMA pipe (FA4-style degree-3 polynomial on the fractional part,
-// exponent by integer add): relieves the MUFU pipe for a share of the columns.
-// Only FMA/ALU-pipe instructions (no FRND/F2I, which share the MUFU/XU pipe):
-// round-to-nearest via the 1.5*2^23 magic constant, f in [-0.5, 0.5], degree-4
-// polynomial for 2^f (rel. error < 2e-5, far below bf16's 4e-3), exponent added
-// as an integer shift.
-__device__ __forceinline__ float ex2_poly(float x) {
-    x = fmaxf(x, -126.f);
-    const float t = x + 12582912.f;   // 1.5 * 2^23: integer part lands in the low mantissa bits
-    const float f = x - (t - 12582912.f);
-    float p = fmaf(0.0096181291f, f, 0.0555041087f);
-    p = fmaf(p, f, 0.2402265070f);
-    p = fmaf(p, f, 0.6931471806f);
-    p = fmaf(p, f, 1.0f);
-    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+// exp2 of a PAIR on the FMA pipe (packed f32x2 ops, FA4-style): round-to-nearest via
+// the 1.5*2^23 magic constant, f = x - round(x) in [-0.5, 0.5], degree-3 minimax
+// polynomial for 2^f (max rel. error 8e-5, far below bf16's 3.9e-3), exponent added
+// as an integer.  Per pair: 2 FMNMX (clamp, ALU) + 6 packed FADD2/FFMA2 + 2 integer
+// adds, instead of 2 MUFU.EX2 — it relieves the MUFU pipe, which is co-critical with
+// the tensor pipe (2 x 128 x 128 exp2 per CTA and key block = 2048 cycles at 16/clk/SM,
+// the same as the block's four 128^3 MMAs).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -126.f);
+    x.y = fmaxf(x.y, -126.f);
+    const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+    const float2 t = __fadd2_rn(x, magic);                       // round(x) in the low mantissa bits
+    const float2 fl = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = __ffma2_rn(fl, make_float2(-1.f, -1.f), x);
+    float2 p = __ffma2_rn(f, make_float2(0.05516013875603676f, 0.05516013875603676f),
+                          make_float2(0.2425827533006668f, 0.2425827533006668f));
+    p = __ffma2_rn(p, f, make_float2(0.6932605504989624f, 0.6932605504989624f));
+    p = __ffma2_rn(p, f, make_float2(0.999930202960968f, 0.999930202960968f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-template <int POLY>
+// Debug timeline (TR variant only): clock64() stamps of CTA (0,0,0), indexed
+// [(j * 2 + tile) * 8 + event] for the first 64 key blocks.  Events: 0 S ready (softmax),
+// 1 row max done, 2 p_half arrived, 3 p_full arrived, 4 MMA saw p_half, 5 MMA saw p_full,
+// 6 MMA issued S(j+1).
+__device__ unsigned long long* g_attn_trace = nullptr;
+
+template <bool TR>
+__device__ __forceinline__ void trace_ev(int j, int t, int ev) {
+    if (TR && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && j < 64 && g_attn_trace)
+        g_attn_trace[(j * 2 + t) * 8 + ev] = clock64();
+}
+
+// One 128-key block of the online softmax for one query row (the calling thread's TMEM
+// lane): pass 1 row max over S (all 128 columns in flight), lazy O rescale, pass 2
+// re-reads S 64 columns at a time (registers stay free for the exponentials' ILP) and
+// writes P = exp2(s*c - m*c) as packed bf16 over S's first 64 columns, published in two
+// halves (p_half after keys [0,64), p_full after [64,128)) so the MMA warp starts
+// O += P[:, :64] V[:64] while the second half is computed.  POLY of every 16 pairs use
+// the FMA-pipe polynomial, the rest MUFU.EX2.  MASK: keys >= valid get probability 0.
+template <int POLY, bool MASK, bool TR>
+__device__ __forceinline__ void softmax_block(uint32_t tS, uint32_t tO, int valid, float c, float& m_run,
+                                              float& l_run, uint64_t* p_half, uint64_t* p_full, int j, int t,
+                                              bool tr0) {
+    float mx;
+    {
+        uint32_t r[kTile];
+#pragma unroll
+        for (int cc = 0; cc < kTile; cc += 32) tmem_ld32(tS + cc, *reinterpret_cast<uint32_t(*)[32]>(r + cc));
+        tmem_ld_wait();
+        if (MASK) {
+#pragma unroll
+            for (int u = 0; u < kTile; ++u)
+                if (u >= valid) r[u] = __float_as_uint(-INFINITY);
+        }
+        float m8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) m8[u] = __uint_as_float(r[u]);
+#pragma unroll
+        for (int u = 8; u < kTile; ++u) m8[u & 7] = fmaxf(m8[u & 7], __uint_as_float(r[u]));
+        mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+    }
+    if (tr0) trace_ev<TR>(j, t, 1);
+    // lazy rescale: keep the stale max unless it grew by more than 8 (log2 units)
+    const bool need = m_run == -INFINITY || (mx - m_run) * c > 8.f;
+    if (__any_sync(0xffffffff, need && m_run != -INFINITY)) {
+        // O_t(j-1) is final: S_t(j) was issued after it and has completed
+        const float alpha = need && m_run != -INFINITY ? ex2((m_run - mx) * c) : 1.f;
+#pragma unroll 1
+        for (int cc = 0; cc < kHD; cc += 32) {
+            uint32_t r[32];
+            tmem_ld32(tO + cc, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int u = 0; u < 32; ++u) r[u] = __float_as_uint(__uint_as_float(r[u]) * alpha);
+            tmem_st32(tO + cc, r);
+        }
+        l_run *= alpha;
+    }
+    if (need) m_run = mx;
+    const float2 c2 = make_float2(c, c), nmc2 = make_float2(-m_run * c, -m_run * c);
+    float2 lsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+    for (int hc = 0; hc < kTile; hc += 64) {
+        uint32_t r[64];
+        tmem_ld32(tS + hc, *reinterpret_cast<uint32_t(*)[32]>(r));
+        tmem_ld32(tS + hc + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+        tmem_ld_wait();
+        if (MASK) {
+#pragma unroll
+            for (int u = 0; u < 64; ++u)
+                if (hc + u >= valid) r[u] = __float_as_uint(-INFINITY);
+        }
+#pragma unroll
+        for (int cc = 0; cc < 64; cc += 32) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const float2 sx = make_float2(__uint_as_float(r[cc + 2 * u]), __uint_as_float(r[cc + 2 * u + 1]));
+                const float2 x = __ffma2_rn(sx, c2, nmc2);
+                float2 p;
+                if (POLY > 0 && ((u * 5) & 15) < POLY) {  // spread the polynomial pairs over the chunk
+                    p = ex2_poly2(x);
+                } else {
+                    p.x = ex2(x.x);
+                    p.y = ex2(x.y);
+                }
+                lsum[u & 1] = __fadd2_rn(lsum[u & 1], p);
+                pk[u] = pack_bf16(p.x, p.y);
+            }
+            tmem_st16(tS + (hc + cc) / 2, pk);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(hc == 0 ? p_half : p_full);
+        if (tr0) trace_ev<TR>(j, t, hc == 0 ? 2 : 3);
+    }
+    const float2 ls = __fadd2_rn(lsum[0], lsum[1]);
+    l_run += ls.x + ls.y;
+}
+
+template <int POLY, bool TR = false>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     k_attention(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                 const __grid_constant__ CUtensorMap tv, AttnKernelArgs a) {
@@ -156,6 +261,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         if (lane == 0) {
             constexpr uint32_t idS = idesc_bf16(128, 128);
             constexpr uint32_t idO = idesc_bf16(128, 128, /*b_mn_major=*/true);
+            // descriptors built once; per-k offsets go into the start-address field (addr >> 4)
+            const uint64_t dQ = desc_sw128(smem_u32(sQ)), dK = desc_sw128(smem_u32(sK));
+            const uint64_t dV = desc_sw128(smem_u32(sV), /*sbo=*/1024, /*lbo=*/kAtom);
             mbar_wait(q_full, 0);
             auto issue_s = [&](int t, int j) {
                 const int s = j % kKStages;
@@ -163,23 +271,22 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     mbar_wait(&k_full[s], (j / kKStages) & 1);
                     tc_fence_after();
                 }
-                const uint32_t q0 = smem_u32(sQ + t * kTileBytes), k0 = smem_u32(sK + s * kTileBytes);
+                const uint64_t q0 = dQ + t * (kTileBytes >> 4), k0 = dK + s * (kTileBytes >> 4);
 #pragma unroll
                 for (int k = 0; k < kHD / 16; ++k) {
-                    const uint32_t off = (k >> 2) * kAtom + (k & 3) * 32;
-                    mma_ss(tmem + t * 128, desc_sw128(q0 + off), desc_sw128(k0 + off), idS, k != 0);
+                    const uint64_t off = static_cast<uint64_t>((k >> 2) * kAtom + (k & 3) * 32) >> 4;
+                    mma_ss(tmem + t * 128, q0 + off, k0 + off, idS, k != 0);
                 }
                 mma_commit(&s_full[t]);
                 if (t == 1) mma_commit(&k_empty[s]);  // both tiles' S issued: K_j slot frees on completion
             };
             auto issue_pv = [&](int t, int j, int half) {
-                const uint32_t v0 = smem_u32(sV + (j % kVStages) * kTileBytes);
+                const uint64_t v0 = dV + (j % kVStages) * (kTileBytes >> 4);
 #pragma unroll
                 for (int k = half * 4; k < half * 4 + 4; ++k) {
                     // A = P_t (TMEM, bf16 pairs: 8 columns per 16 kv); B = V [kv][d] MN-major:
                     // 16 kv rows per step (2048 B), d halves LBO = 16 KB apart
-                    mma_ts(tmem + 256 + t * 128, tmem + t * 128 + k * 8,
-                           desc_sw128(v0 + k * 2048, /*sbo=*/1024, /*lbo=*/kAtom), idO, (j | k) != 0);
+                    mma_ts(tmem + 256 + t * 128, tmem + t * 128 + k * 8, v0 + ((k * 2048) >> 4), idO, (j | k) != 0);
                 }
             };
             issue_s(0, 0);
@@ -189,14 +296,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 for (int t = 0; t < 2; ++t) {
                     mbar_wait(&p_half[t], j & 1);
                     if (t == 0) mbar_wait(&v_full[j % kVStages], (j / kVStages) & 1);
+                    trace_ev<TR>(j, t, 4);
                     tc_fence_after();
                     issue_pv(t, j, 0);
                     mbar_wait(&p_full[t], j & 1);
+                    trace_ev<TR>(j, t, 5);
                     tc_fence_after();
                     issue_pv(t, j, 1);
                     if (!more) mma_commit(&o_final[t]);
                     if (t == 1) mma_commit(&v_empty[j % kVStages]);
                     if (more) issue_s(t, j + 1);
+                    trace_ev<TR>(j, t, 6);
                 }
             }
         }
@@ -211,72 +321,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         float m_run = -INFINITY, l_run = 0.f;
         for (int j = 0; j < nkv; ++j) {
             mbar_wait(&s_full[t], j & 1);
+            const bool tr0 = TR && (warp & 3) == 2 && lane == 0;
+            if (tr0) trace_ev<TR>(j, t, 0);
             tc_fence_after();
-            float sv[kTile];
-#pragma unroll
-            for (int cc = 0; cc < kTile; cc += 32) {
-                uint32_t r[32];
-                tmem_ld32(tS + cc, r);
-#pragma unroll
-                for (int u = 0; u < 32; ++u) sv[cc + u] = __uint_as_float(r[u]);
-            }
-            tmem_ld_wait();
             const int valid = static_cast<int>(a.n_kv - static_cast<int64_t>(j) * kTile);
-            if (valid < kTile) {
-#pragma unroll
-                for (int u = 0; u < kTile; ++u)
-                    if (u >= valid) sv[u] = -INFINITY;
-            }
-            // row max as an 8-way tree (a 127-long FMNMX chain is pure latency)
-            float m8[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) m8[u] = sv[u];
-#pragma unroll
-            for (int u = 8; u < kTile; ++u) m8[u & 7] = fmaxf(m8[u & 7], sv[u]);
-            const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                                   fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-            // lazy rescale: keep the stale max unless it grew by more than 8 (log2 units)
-            const bool need = m_run == -INFINITY || (mx - m_run) * c > 8.f;
-            if (__any_sync(0xffffffff, need && m_run != -INFINITY)) {
-                // O_t(j-1) is final: S_t(j) was issued after it and has completed
-                const float alpha = need && m_run != -INFINITY ? ex2((m_run - mx) * c) : 1.f;
-#pragma unroll 1
-                for (int cc = 0; cc < kHD; cc += 32) {
-                    uint32_t r[32];
-                    tmem_ld32(tO + cc, r);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int u = 0; u < 32; ++u) r[u] = __float_as_uint(__uint_as_float(r[u]) * alpha);
-                    tmem_st32(tO + cc, r);
-                }
-                l_run *= alpha;
-            }
-            if (need) m_run = mx;
-            const float mc = m_run * c;
-            float lsum[4] = {0.f, 0.f, 0.f, 0.f};
-            // P = exp2(s*c - m*c) -> packed bf16 into S_t's first 64 columns
-            // published in two halves: the MMA warp starts O += P[:, :64] V[:64] while the
-            // second half of the exponentials is still being computed
-#pragma unroll
-            for (int cc = 0; cc < kTile; cc += 32) {
-                uint32_t pk[16];
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const bool poly = POLY > 0 && (u % 8) < POLY;
-                    const float x0 = fmaf(sv[cc + 2 * u], c, -mc), x1 = fmaf(sv[cc + 2 * u + 1], c, -mc);
-                    const float p0 = poly ? ex2_poly(x0) : ex2(x0);
-                    const float p1 = poly ? ex2_poly(x1) : ex2(x1);
-                    lsum[u & 3] += p0 + p1;  // 4 independent partial sums
-                    pk[u] = pack_bf16(p0, p1);
-                }
-                tmem_st16(tS + cc / 2, pk);
-                if (cc == 32 || cc == 96) {
-                    tmem_st_wait();
-                    tc_fence_before();
-                    mbar_arrive(cc == 32 ? &p_half[t] : &p_full[t]);
-                }
-            }
-            l_run += (lsum[0] + lsum[1]) + (lsum[2] + lsum[3]);
+            // the ragged last key block takes a separately compiled masked copy, so full
+            // blocks carry no per-element compare/select
+            if (valid >= kTile)
+                softmax_block<POLY, false, TR>(tS, tO, valid, c, m_run, l_run, &p_half[t], &p_full[t], j, t, tr0);
+            else
+                softmax_block<POLY, true, TR>(tS, tO, valid, c, m_run, l_run, &p_half[t], &p_full[t], j, t, tr0);
         }
         // epilogue: O_t / l -> bf16 rows
         mbar_wait(&o_final[t], 0);
@@ -306,17 +360,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 }
 
 static int attn_poly() {
-    const int v = tune_get("attn_poly", 0);  // eighths of the exponentials on the FMA pipe (A/B: 0 best)
-    return v < 0 || v > 3 ? 0 : v;
+    // pairs out of every 16 whose exp2 runs on the FMA pipe (0, 4, 6 compiled)
+    const int v = tune_get("attn_poly", 4);
+    return v == 0 || v == 6 ? v : 4;
 }
 
 void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         LP_CUDA(cudaFuncSetAttribute(k_attention<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
-        LP_CUDA(cudaFuncSetAttribute(k_attention<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
-        LP_CUDA(cudaFuncSetAttribute(k_attention<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
-        LP_CUDA(cudaFuncSetAttribute(k_attention<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         attr = true;
     }
     if ((x.ldq | x.ldk | x.ldv | x.ldo) % 8) fail(LP_ERR_INVALID_ARGUMENT, "attention: strides must be multiples of 8");
@@ -338,11 +393,11 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     const dim3 grid(static_cast<unsigned>((x.n_q + 2 * kTile - 1) / (2 * kTile)), x.heads, x.batch);
     const int cls = x.n_kv == x.n_q && x.q == x.k ? KC_SELF_ATTN : KC_CROSS_ATTN;
     prof_begin(cls, st);
-    switch (attn_poly()) {
+    switch (tune_get("attn_trace", 0) ? -1 : attn_poly()) {
+        case -1: k_attention<0, true><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
         case 0: k_attention<0><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
-        case 2: k_attention<2><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
-        case 3: k_attention<3><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
-        default: k_attention<1><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
+        case 6: k_attention<6><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
+        default: k_attention<4><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
     }
     LP_LAUNCH_CHECK();
     prof_end(cls, st, 4.0 * x.batch * x.heads * static_cast<double>(x.n_q) * static_cast<double>(x.n_kv) * kHD,
@@ -352,6 +407,11 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
 }  // namespace lpb200
 
 using namespace lpb200;
+
+// Debug: device buffer of 64*2*8 u64 receiving the TR variant's timeline (lp_tune("attn_trace", 1)).
+extern "C" int lp_attention_set_trace(void* dev_buf) {
+    return guard([&] { LP_CUDA(cudaMemcpyToSymbol(g_attn_trace, &dev_buf, sizeof(void*))); });
+}
 
 // q,k,v,o: [B, S, H, 128] bf16 contiguous
 extern "C" int lp_attention_bf16(const void* q, const void* k, const void* v, void* o, int64_t batch, int64_t seq_q,

@@ -53,15 +53,17 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-// Watchdog: a wait still pending after 10 s of wall time traps, so a protocol
-// bug surfaces as a launch error instead of a hung GPU.
+// Watchdog: a wait still pending after ~2^35 SM cycles (>= 17 s at 1.965 GHz) traps, so
+// a protocol bug surfaces as a launch error instead of a hung GPU.  clock64 (CS2R) is
+// cheap; %globaltimer reads on every missed first try cost hundreds of cycles on the
+// critical MMA-issue path (r1g attention timeline).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     if (mbar_try_wait(a, parity)) return;
-    const uint64_t t0 = globaltimer_ns();
+    const long long t0 = clock64();
     uint32_t n = 0;
     while (!mbar_try_wait(a, parity)) {
-        if ((++n & 255) == 0 && globaltimer_ns() - t0 > 10000000000ull) __trap();
+        if ((++n & 1023) == 0 && clock64() - t0 > (1ll << 35)) __trap();
     }
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {

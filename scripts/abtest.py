@@ -31,6 +31,18 @@ def run(S):
                                    C.c_void_p(o.data_ptr()), 2, S, S, 12, 1 / 128 ** 0.5, st()))
 
 
+# correctness of every variant against torch SDPA (fp32 softmax) at the first size
+err = {}
+S0 = 3000  # not a multiple of 128: exercises the key mask; small enough for an fp32 SDPA reference
+bufs[S0] = [torch.randn(2, S0, 12, 128, device="cuda").bfloat16() for _ in range(4)]
+q, k, v, o = bufs[S0]
+ref = torch.nn.functional.scaled_dot_product_attention(*(x.transpose(1, 2).float() for x in (q, k, v))).transpose(1, 2)
+for v_ in variants:
+    _lib.check(L.lp_tune(knob.encode(), v_))
+    run(S0)
+    torch.cuda.synchronize()
+    err[v_] = float((o.float() - ref).abs().max())
+del ref
 for rnd in range(6):
     for S in sizes:
         for v in variants:
@@ -48,4 +60,4 @@ out = {}
 for S in sizes:
     fl = 4 * 2 * 12 * S * S * 128
     out[S] = {v: round(fl / statistics.median(res[(v, S)]) / 1e9, 1) for v in variants}
-print(json.dumps({"knob": knob, "tflops": out}))
+print(json.dumps({"knob": knob, "tflops": out, "max_abs_err_vs_sdpa": err}))

@@ -154,6 +154,33 @@ int lp_cost_report(int steps, int workers, double overlap_ratio, const int64_t s
                    int64_t hidden_dim, int wire_bytes, int hybrid_groups, const int32_t* group_sizes,
                    lp_cost_report_t* out);
 
+/* N-completeness checker — verify_n_complete (src/completeness.cpp:104-160,
+ * include/lpsim/completeness.hpp:8-92), host side.  grid = patch-grid {nt, nh, nw};
+ * schedule[i] = axis of step i+1 (lp_axis), schedule_len >= budget.  max_positions = 0
+ * keeps the reference's 4096-position cap (InvalidArgument beyond it), > 0 lifts it.
+ * min_steps_out (nt*nh*nw int32, or NULL): first step at which each position is complete, -1 never. */
+int lp_verify_n_complete(const int64_t grid[3], int32_t workers, double overlap_ratio, const int32_t* schedule,
+                         int32_t schedule_len, int32_t budget, int64_t max_positions, int32_t* complete_out,
+                         int32_t* complete_at_out, int64_t worst_out[3], int32_t* min_steps_out);
+/* Per-step coverage rows of the completeness command (src/commands.cpp:169-195):
+ * rows_i[5*s..] = {step, min_reached, max_reached, complete_positions, total_positions},
+ * rows_mean[s] = mean_reached; stops after the first all-complete step. */
+int lp_coverage_trace(const int64_t grid[3], int32_t workers, double overlap_ratio, const int32_t* schedule,
+                      int32_t schedule_len, int32_t budget, int64_t max_positions, int64_t* rows_i, double* rows_mean,
+                      int32_t* n_rows_out);
+
+/* LPLT latent dump — write_latent_dump / read_latent_dump (src/io.cpp:37-139).  `bits` are
+ * the storage-dtype bits (f16 / f32 / f64, little-endian) of a row-major (c,t,h,w) latent —
+ * exactly what the engine holds on the device.  read: bits = NULL parses the header only. */
+int lp_latent_dump_write(const char* path, const void* bits, const int64_t shape[4], int32_t dtype_bytes);
+int lp_latent_dump_read(const char* path, int64_t shape_out[4], int32_t* dtype_bytes_out, void* bits,
+                        int64_t capacity_bytes);
+
+/* The `lpsim` command line (tools/lpsim_main.cpp:42-113, src/commands.cpp:46-216) on this
+ * engine: simulate | compare | cost | completeness | partition-plan, --config/--out/--seed/
+ * --quiet (+ --backend b200).  Returns the process exit code: 0, 2 (config/usage), 3. */
+int lp_cli_main(int argc, const char* const* argv);
+
 /* Quantizer (src/dtype.cpp:34-116), host side, for tests and host shims. */
 uint16_t lp_f16_encode(double v);
 double lp_f16_decode(uint16_t bits);

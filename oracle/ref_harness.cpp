@@ -13,12 +13,15 @@
 //   entries[9n] = {k, core_b, core_e, ext_b, ext_e, lat_b, lat_e, delta_s, delta_e}
 
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "lpsim/cluster.hpp"
+#include "lpsim/commands.hpp"
+#include "lpsim/io.hpp"
 #include "lpsim/completeness.hpp"
 #include "lpsim/cost.hpp"
 #include "lpsim/denoise.hpp"
@@ -363,6 +366,41 @@ int ref_verify_n_complete(const int64_t* grid, int workers, double r, const int*
         out[2] = res.worst.t;
         out[3] = res.worst.h;
         out[4] = res.worst.w;
+    });
+}
+
+// The reference's command layer (src/commands.cpp:46-216) — what its CLI runs
+// (tools/lpsim_main.cpp:95-104, which needs the absent CLI11): load_run_config + the
+// command, artifacts written into out_dir, the returned summary as dump(2) into buf.
+// seed < 0: keep the config's seed.  cmd: simulate | compare | cost | completeness | partition-plan.
+int ref_command(const char* cmd, const char* config, const char* out_dir, int64_t seed, const char* schedule,
+                int max_steps, int step, char* buf, int64_t cap) {
+    return guarded([&] {
+        RunConfig cfg = load_run_config(config);
+        if (out_dir && *out_dir) cfg.output.dir = out_dir;
+        if (seed >= 0) cfg.denoiser.seed = static_cast<std::uint64_t>(seed);
+        const std::string c = cmd;
+        nlohmann::json s;
+        if (c == "simulate") s = simulate_run(cfg);
+        else if (c == "compare") s = compare_run(cfg);
+        else if (c == "cost") s = cost_run(cfg);
+        else if (c == "completeness") s = completeness_run(cfg, schedule, max_steps);
+        else s = partition_plan_run(cfg, step);
+        const std::string d = s.dump(2);
+        std::snprintf(buf, static_cast<size_t>(cap), "%s", d.c_str());
+    });
+}
+
+// write_latent_dump / read_latent_dump (src/io.cpp:37-139) on doubles.
+int ref_save_latent(const char* path, const double* v, const int64_t* shape, int dtype_bytes) {
+    return guarded([&] { write_latent_dump(path, to_tensor(v, shape, dtype_bytes)); });
+}
+int ref_load_latent(const char* path, int64_t* shape_out, int* dtype_out, double* v_out) {
+    return guarded([&] {
+        const LatentTensor z = read_latent_dump(path);
+        shape_out[0] = z.shape().c, shape_out[1] = z.shape().t, shape_out[2] = z.shape().h, shape_out[3] = z.shape().w;
+        *dtype_out = dtype_bytes(z.dtype());
+        if (v_out) copy_out(z, v_out);
     });
 }
 

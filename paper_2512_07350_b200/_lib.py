@@ -124,6 +124,12 @@ _SIGS = {
     "lp_gemm_bf16": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "lp_attention_bf16": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _d, _vp]),
     "lp_attention_set_trace": (_i, [_vp]),
+    "lp_verify_n_complete": (_i, [_i64p, _i32, _d, C.POINTER(_i32), _i32, _i32, _i64, C.POINTER(_i32),
+                                  C.POINTER(_i32), _i64p, C.POINTER(_i32)]),
+    "lp_coverage_trace": (_i, [_i64p, _i32, _d, C.POINTER(_i32), _i32, _i32, _i64, _i64p, _f64p, C.POINTER(_i32)]),
+    "lp_latent_dump_write": (_i, [C.c_char_p, _vp, _i64p, _i32]),
+    "lp_latent_dump_read": (_i, [C.c_char_p, _i64p, C.POINTER(_i32), _vp, _i64]),
+    "lp_cli_main": (_i, [_i, C.POINTER(C.c_char_p)]),
     "lp_nccl_unique_id": (_i, [C.POINTER(C.c_uint8 * 128)]),
     "lp_engine_create": (_i, [C.POINTER(EngineConfig), _vp, _f64p, _i32, C.POINTER(_vp)]),
     "lp_engine_destroy": (_i, [_vp]),

@@ -33,12 +33,23 @@ SOURCES = [
     ("attn_tcgen05.cu", []),
     ("dit.cpp", []),
     ("engine.cpp", ["-Xcompiler", "-ffp-contract=off"]),
+    ("completeness.cpp", []),
+    ("commands.cpp", None),  # host-only (g++): the lpsim command layer, nlohmann/json
 ]
+GXX = shutil.which("g++") or "g++"
+CUDA_INC = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(NVCC))), "include")
+# nlohmann/json 3.11.3 — the header the reference's own build uses (vendored by cudnn_frontend in this image)
+JSON_INC = os.path.join(sys.prefix, "lib", f"python{sys.version_info.major}.{sys.version_info.minor}", "site-packages",
+                        "include", "cudnn_frontend", "thirdparty", "nlohmann")
+CLI = os.path.join(PKG, "lpsim_b200")
 
 
 def _cmd(src, extra):
     path = os.path.join(CSRC, src)
     obj = os.path.join(OUT, src + ".o")
+    if extra is None:  # host-only C++
+        return path, obj, [GXX, "-std=c++17", "-O2", "-fPIC", "-I" + CUDA_INC, "-I" + JSON_INC, *INCS, "-c", path,
+                           "-o", obj]
     lang = ["-x", "cu"]  # .cpp too: they share the device codec header
     cmd = [NVCC, *lang, "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", "-Xptxas", "-v",
            "--expt-relaxed-constexpr", *INCS, *extra, "-c", path, "-o", obj]
@@ -88,6 +99,11 @@ def build(verbose: bool = False, force: bool = False) -> str:
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stderr[-8000:])
+    cli = [GXX, "-O2", os.path.join(CSRC, "lpsim_main.cpp"), "-o", CLI, "-L" + PKG, "-llp_b200",
+           "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cli, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("CLI link failed:\n" + r.stderr[-8000:])
     return LIB
 
 

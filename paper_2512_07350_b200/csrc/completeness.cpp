@@ -17,7 +17,6 @@
 // The reference caps the analysis at 4096 positions (kMaxGridPositions) and rejects
 // larger grids with InvalidArgument; `max_positions` = 0 keeps that cap, a larger value
 // lifts it (the BASELINE C5 grid is 41 x 30 x 52 = 63,960 positions).
-#include <bit>
 #include <cstring>
 #include <vector>
 
@@ -58,7 +57,7 @@ struct Reach {
     i64 count(i64 p) const {
         i64 c = 0;
         const uint64_t* r = row(p);
-        for (i64 i = 0; i < words; ++i) c += std::popcount(r[i]);
+        for (i64 i = 0; i < words; ++i) c += __builtin_popcountll(r[i]);
         return c;
     }
 };

@@ -24,7 +24,7 @@ __all__ = [
     "weight_profile", "synthetic_latent", "extract_sublatents", "BoxDenoiser", "GlobalMixDenoiser",
     "IdentityDenoiser", "DiTDenoiser", "cfg_predict", "sampler_step", "reconstruct", "reconstruct_update",
     "run_lp", "run_centralized", "LpEngine", "quantize", "f16_encode", "step_comm_bytes", "shard_layout",
-    "PRESETS",
+    "PRESETS", "presets", "verify_n_complete", "save_latent", "load_latent", "cli",
 ]
 
 # ModelPreset (src/latent.cpp:197-205): wire width used by the comm ledger.
@@ -592,3 +592,59 @@ def run_centralized(denoiser, radius, z: LatentTensor, steps, eta, guidance, con
     """run_centralized (src/denoise.cpp:158-174) ≡ run_lp at K=1 (test_cluster.cpp:75-92)."""
     out, _ = run_lp(denoiser, radius, z, steps, eta, guidance, cond, (1, 1, 1), 1, 0.0, dit=dit)
     return out
+
+
+# --------------------------------------------------------------------------
+# Completeness, latent dumps, presets, CLI (SURVEY.md §8 f1/f3/f4)
+# --------------------------------------------------------------------------
+def presets():
+    """builtin_presets (src/latent.cpp:197-206), as the binding's presets() (lpsim_bindings.cpp:277-289)."""
+    return [{"name": k, "hidden_dim": v["hidden_dim"], "dtype_bytes": v["dtype_bytes"]} for k, v in PRESETS.items()]
+
+
+def verify_n_complete(grid, workers, overlap_ratio, schedule="rotating", budget=8, max_positions=0):
+    """verify_n_complete (src/completeness.cpp:104-160) with the binding's signature
+    (lpsim_bindings.cpp:247-271); `schedule` may also be an explicit axis list / string
+    ("TTHTTW", repeated cyclically).  Returns {complete, complete_at, worst_position, min_steps}."""
+    if isinstance(schedule, str) and schedule in ("rotating", "temporal", "height", "width"):
+        axes = [rotation_axis(i) for i in range(1, budget + 1)] if schedule == "rotating" else \
+            [int(Axis[schedule])] * budget
+    else:
+        cyc = parse_schedule(schedule)
+        axes = [cyc[i % len(cyc)] for i in range(budget)]
+    n = int(grid[0]) * int(grid[1]) * int(grid[2])
+    sched = (C.c_int32 * len(axes))(*axes)
+    comp, at = C.c_int32(), C.c_int32()
+    worst = (C.c_int64 * 3)()
+    mins = (C.c_int32 * max(n, 1))()
+    check(lib().lp_verify_n_complete(i64arr(grid), int(workers), float(overlap_ratio), sched, len(axes), int(budget),
+                                     int(max_positions), C.byref(comp), C.byref(at), worst, mins))
+    return {"complete": bool(comp.value), "complete_at": at.value if comp.value else None,
+            "worst_position": (worst[0], worst[1], worst[2]), "min_steps": list(mins[:n])}
+
+
+def save_latent(path, tensor: LatentTensor):
+    """write_latent_dump (src/io.cpp:39-79): LPLT header + storage-width payload."""
+    host = tensor.data.contiguous().cpu()
+    check(lib().lp_latent_dump_write(str(path).encode(), C.c_void_p(host.data_ptr()), i64arr(tensor.shape),
+                                     tensor.dtype_bytes))
+
+
+def load_latent(path, device="cuda") -> LatentTensor:
+    """read_latent_dump (src/io.cpp:81-139)."""
+    torch = _torch()
+    shape, db = (C.c_int64 * 4)(), C.c_int32()
+    check(lib().lp_latent_dump_read(str(path).encode(), shape, C.byref(db), None, 0))
+    dims = tuple(shape)
+    dt = getattr(torch, _TORCH_DT[db.value])
+    host = torch.empty(dims, dtype=dt)
+    check(lib().lp_latent_dump_read(str(path).encode(), shape, C.byref(db), C.c_void_p(host.data_ptr()),
+                                    host.numel() * db.value))
+    return LatentTensor(host.to(device) if device else host, db.value)
+
+
+def cli(argv):
+    """The `lpsim` command line on this engine (lp_cli_main); returns the exit code."""
+    args = ["lpsim_b200", *[str(a) for a in argv]]
+    arr = (C.c_char_p * len(args))(*[a.encode() for a in args])
+    return lib().lp_cli_main(len(args), arr)

@@ -63,3 +63,42 @@ def test_engine_custom_schedule_bitexact(cuda, oracle):
         got, _ = lp.run_lp("box", (1, 1, 1), lp.LatentTensor.from_numpy(z, d), steps, 0.05, 3.0, list(cond), patch, K, r,
                            schedule=TEMPORAL_HEAVY)
         assert np.array_equal(got.to_numpy(), want)
+
+
+def test_verify_n_complete_matches_reference_sweep(reference):
+    """Our C++ checker (completeness.cpp) vs the reference's verify_n_complete on random
+    grids, worker counts, overlap ratios and schedules (rotating, constant, custom)."""
+    rng = np.random.default_rng(5)
+    scheds = ["rotating", "temporal", "height", "width", "TTHTTW", "HW", "TWH"]
+    for _ in range(60):
+        grid = tuple(int(x) for x in rng.integers(1, 12, 3))
+        K = int(rng.integers(1, 6))
+        r = float(rng.choice([0.0, 0.25, 0.5, 1.0])) if K > 1 else 0.0
+        r = min(r, K - 1)
+        name = str(rng.choice(scheds))
+        budget = int(rng.integers(1, 10))
+        got = lp.verify_n_complete(grid, K, r, name, budget)
+        if name == "rotating":
+            axes = [lp.rotation_axis(i) for i in range(1, budget + 1)]
+        elif name in ("temporal", "height", "width"):
+            axes = [int(lp.Axis[name])] * budget
+        else:
+            cyc = lp.parse_schedule(name)
+            axes = [cyc[i % len(cyc)] for i in range(budget)]
+        want = verify_n_complete(reference, grid, K, r, axes, budget)
+        assert (got["complete"], got["complete_at"], tuple(got["worst_position"])) == \
+            (want["complete"], want["complete_at"], want["worst_position"]), (grid, K, r, name, budget)
+
+
+def test_verify_n_complete_cap_and_lifted_cap():
+    # the reference caps exhaustive analysis at 4096 positions (src/completeness.cpp:13,35-40)
+    with pytest.raises(lp.LpError) as e:
+        lp.verify_n_complete((17, 16, 16), 4, 0.5, "rotating", 8)
+    assert e.value.status == 10 and "capped at 4096" in str(e.value)  # InvalidArgument
+    # lifted: a C5-like grid (161 frames -> 41 latent frames, halved H/W patch grid) with the
+    # temporal-heavy schedule is N-complete; so is the rotation
+    grid = (41, 15, 26)
+    th = lp.verify_n_complete(grid, 8, 0.5, TEMPORAL_HEAVY, 12, max_positions=grid[0] * grid[1] * grid[2])
+    rot = lp.verify_n_complete(grid, 8, 0.5, "rotating", 12, max_positions=grid[0] * grid[1] * grid[2])
+    assert th["complete"] and rot["complete"]
+    assert th["complete_at"] <= 12 and min(th["min_steps"]) >= 1

@@ -133,40 +133,51 @@ __device__ __forceinline__ void softmax_block(uint32_t tS, uint32_t tO, int vali
     const float2 c2 = make_float2(c, c), nmc2 = make_float2(-m_run * c, -m_run * c);
     float2 lsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-    for (int hc = 0; hc < kTile; hc += 64) {
-        uint32_t r[64];
-        tmem_ld32(tS + hc, *reinterpret_cast<uint32_t(*)[32]>(r));
-        tmem_ld32(tS + hc + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
-        tmem_ld_wait();
-        if (MASK) {
+    // 32-column chunks, the next chunk's TMEM load in flight while this one is computed
+    // (register double buffer; LDTM results are scoreboard-tracked)
+    auto chunk = [&](const uint32_t (&r)[32], int cc) {
+        uint32_t pk[16];
 #pragma unroll
-            for (int u = 0; u < 64; ++u)
-                if (hc + u >= valid) r[u] = __float_as_uint(-INFINITY);
-        }
-#pragma unroll
-        for (int cc = 0; cc < 64; cc += 32) {
-            uint32_t pk[16];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                const float2 sx = make_float2(__uint_as_float(r[cc + 2 * u]), __uint_as_float(r[cc + 2 * u + 1]));
-                const float2 x = __ffma2_rn(sx, c2, nmc2);
-                float2 p;
-                if (POLY > 0 && ((u * 5) & 15) < POLY) {  // spread the polynomial pairs over the chunk
-                    p = ex2_poly2(x);
-                } else {
-                    p.x = ex2(x.x);
-                    p.y = ex2(x.y);
-                }
-                lsum[u & 1] = __fadd2_rn(lsum[u & 1], p);
-                pk[u] = pack_bf16(p.x, p.y);
+        for (int u = 0; u < 16; ++u) {
+            float2 sx = make_float2(__uint_as_float(r[2 * u]), __uint_as_float(r[2 * u + 1]));
+            if (MASK) {
+                if (cc + 2 * u >= valid) sx.x = -INFINITY;
+                if (cc + 2 * u + 1 >= valid) sx.y = -INFINITY;
             }
-            tmem_st16(tS + (hc + cc) / 2, pk);
+            const float2 x = __ffma2_rn(sx, c2, nmc2);
+            float2 p;
+            if (POLY > 0 && ((u * 5) & 15) < POLY) {  // spread the polynomial pairs over the chunk
+                p = ex2_poly2(x);
+            } else {
+                p.x = ex2(x.x);
+                p.y = ex2(x.y);
+            }
+            lsum[u & 1] = __fadd2_rn(lsum[u & 1], p);
+            pk[u] = pack_bf16(p.x, p.y);
         }
+        tmem_st16(tS + cc / 2, pk);
+    };
+    auto publish = [&](uint64_t* bar, int half) {
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(hc == 0 ? p_half : p_full);
-        if (tr0) trace_ev<TR>(j, t, hc == 0 ? 2 : 3);
-    }
+        mbar_arrive(bar);
+        if (tr0) trace_ev<TR>(j, t, 2 + half);
+    };
+    uint32_t ra[32], rb[32];
+    tmem_ld32(tS, ra);
+    tmem_ld_wait();
+    tmem_ld32(tS + 32, rb);
+    chunk(ra, 0);
+    tmem_ld_wait();
+    tmem_ld32(tS + 64, ra);
+    chunk(rb, 32);
+    publish(p_half, 0);
+    tmem_ld_wait();
+    tmem_ld32(tS + 96, rb);
+    chunk(ra, 64);
+    tmem_ld_wait();
+    chunk(rb, 96);
+    publish(p_full, 1);
     const float2 ls = __fadd2_rn(lsum[0], lsum[1]);
     l_run += ls.x + ls.y;
 }

@@ -187,12 +187,16 @@ __global__ void __launch_bounds__(256) k_layernorm(const float* __restrict__ x, 
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         const int c0 = 4 * (lane + 32 * i);
+        const float4 a4 = reinterpret_cast<const float4*>(a)[lane + 32 * i];
+        const float4 b4 = reinterpret_cast<const float4*>(b)[lane + 32 * i];
+        const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
         float o4[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const float n = (v[4 * i + u] - mean) * rstd;
-            o4[u] = AFFINE ? n * a[c0 + u] + b[c0 + u] : n * (1.f + a[c0 + u]) + b[c0 + u];
+            o4[u] = AFFINE ? n * av[u] + bv[u] : n * (1.f + av[u]) + bv[u];
         }
+        (void)c0;
         __nv_bfloat162 p0 = __floats2bfloat162_rn(o4[0], o4[1]), p1 = __floats2bfloat162_rn(o4[2], o4[3]);
         yr[lane + 32 * i] = make_uint2(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1));
     }
@@ -269,6 +273,114 @@ __global__ void __launch_bounds__(256) k_rmsnorm_rope(__nv_bfloat16* __restrict_
         }
         reinterpret_cast<__nv_bfloat162*>(p)[lane + 32 * i] = __floats2bfloat162_rn(a, b);
     }
+}
+
+// RoPE cos/sin table of one shard grid, computed once per forward with exactly the
+// per-element formula above: [nf x 22 | nh x 21 | nw x 21] float2 (cos, sin).
+__global__ void k_rope_table(float2* __restrict__ tab, int nf, int nh, int nw) {
+    const int total = nf * 22 + nh * 21 + nw * 21;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        int pos, jj, P;
+        if (i < nf * 22) {
+            pos = i / 22, jj = i % 22, P = 22;
+        } else if (i < nf * 22 + nh * 21) {
+            const int k = i - nf * 22;
+            pos = k / 21, jj = k % 21, P = 21;
+        } else {
+            const int k = i - nf * 22 - nh * 21;
+            pos = k / 21, jj = k % 21, P = 21;
+        }
+        const float freq = exp2f(-13.287712379549449f * static_cast<float>(jj) / static_cast<float>(P));
+        float sn, cs;
+        sincosf(static_cast<float>(pos) * freq, &sn, &cs);
+        tab[i] = make_float2(cs, sn);
+    }
+}
+
+// q and k (NSEC = 2 sections of width d at col0 and col0 + d, gains g0 / g1) or one
+// section: RMSNorm over d then 3-D RoPE from the table, in place.  One warp per
+// (row, section); each lane moves 16-byte chunks (8 bf16 = 4 rotation pairs).
+template <int PER8>
+__global__ void __launch_bounds__(256) k_rmsnorm_rope_tab(__nv_bfloat16* __restrict__ buf, int64_t rows, int64_t ld,
+                                                          int64_t col0, int nsec, const float* __restrict__ g0,
+                                                          const float* __restrict__ g1, float eps,
+                                                          const float2* __restrict__ tab, int64_t rows_per_batch,
+                                                          int nf, int nh, int nw) {
+    constexpr int d = PER8 * 256;
+    const int64_t wid = blockIdx.x * 8LL + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = wid / nsec;
+    const int sec = static_cast<int>(wid % nsec);
+    if (row >= rows) return;
+    uint4* p = reinterpret_cast<uint4*>(buf + row * ld + col0 + static_cast<int64_t>(sec) * d);
+    const float* g = sec ? g1 : g0;
+    float v[8 * PER8];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER8; ++i) {
+        const uint4 q = p[lane + 32 * i];
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[u]);
+            v[8 * i + 2 * u] = __bfloat162float(h.x);
+            v[8 * i + 2 * u + 1] = __bfloat162float(h.y);
+            ss += v[8 * i + 2 * u] * v[8 * i + 2 * u] + v[8 * i + 2 * u + 1] * v[8 * i + 2 * u + 1];
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+    const float r = rsqrtf(ss / d + eps);
+    const int64_t tok = row % rows_per_batch;
+    const int px = static_cast<int>(tok % nw), py = static_cast<int>((tok / nw) % nh),
+              pf = static_cast<int>(tok / (static_cast<int64_t>(nw) * nh));
+    const float2* tf = tab + pf * 22;
+    const float2* th = tab + nf * 22 + py * 21 - 22;
+    const float2* tw = tab + nf * 22 + nh * 21 + px * 21 - 43;
+#pragma unroll
+    for (int i = 0; i < PER8; ++i) {
+        const int e = 8 * (lane + 32 * i);
+        const float4 ga = reinterpret_cast<const float4*>(g + e)[0], gb = reinterpret_cast<const float4*>(g + e)[1];
+        const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+        uint32_t w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            float a = v[8 * i + 2 * u] * r * gv[2 * u], b = v[8 * i + 2 * u + 1] * r * gv[2 * u + 1];
+            if (tab) {
+                const int j = ((e & 127) >> 1) + u;  // pair within the head
+                const float2 cs = j < 22 ? tf[j] : (j < 43 ? th[j] : tw[j]);
+                const float a2 = a * cs.x - b * cs.y, b2 = a * cs.y + b * cs.x;
+                a = a2;
+                b = b2;
+            }
+            const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+            w[u] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        p[lane + 32 * i] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+void rope_table(float2* tab, int nf, int nh, int nw, cudaStream_t st) {
+    const int total = nf * 22 + nh * 21 + nw * 21;
+    k_rope_table<<<(total + 255) / 256, 256, 0, st>>>(tab, nf, nh, nw);
+    LP_LAUNCH_CHECK();
+}
+
+bool rmsnorm_rope_tab(__nv_bfloat16* buf, int64_t rows, int64_t ld, int64_t col0, int d, int nsec, const float* g0,
+                      const float* g1, float eps, const float2* tab, int64_t rows_per_batch, int nf, int nh, int nw,
+                      cudaStream_t st) {
+    if (d % 256 || (ld % 8) || (col0 % 8)) return false;
+    const unsigned gr = static_cast<unsigned>((rows * nsec + 7) / 8);
+#define LP_RMT(P)                                                                                                   \
+    if (d == 256 * P) {                                                                                             \
+        k_rmsnorm_rope_tab<P><<<gr, 256, 0, st>>>(buf, rows, ld, col0, nsec, g0, g1, eps, tab, rows_per_batch, nf, nh, \
+                                                  nw);                                                              \
+        LP_LAUNCH_CHECK();                                                                                          \
+        return true;                                                                                                \
+    }
+    LP_RMT(1) LP_RMT(2) LP_RMT(4) LP_RMT(6) LP_RMT(8) LP_RMT(20)
+#undef LP_RMT
+    return false;
 }
 
 void rmsnorm_rope(__nv_bfloat16* buf, int64_t rows, int64_t ld, int64_t col0, int d, const float* g, float eps,

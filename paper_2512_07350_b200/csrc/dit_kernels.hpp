@@ -28,6 +28,13 @@ void layernorm_bf16(const float* x, __nv_bfloat16* y, int64_t rows, int d, const
                     float eps, cudaStream_t st);
 void rmsnorm_rope(__nv_bfloat16* buf, int64_t rows, int64_t ld, int64_t col0, int d, const float* g, float eps,
                   bool rope, int64_t rows_per_batch, int nh, int nw, cudaStream_t st);
+// RoPE cos/sin table [nf*22 + nh*21 + nw*21] float2 of a shard grid (once per forward).
+void rope_table(float2* tab, int nf, int nh, int nw, cudaStream_t st);
+// Table-driven RMSNorm(+RoPE if tab) of nsec adjacent width-d sections (q | k), in place.
+// Returns false when the width / alignment is not covered (callers use rmsnorm_rope).
+bool rmsnorm_rope_tab(__nv_bfloat16* buf, int64_t rows, int64_t ld, int64_t col0, int d, int nsec, const float* g0,
+                      const float* g1, float eps, const float2* tab, int64_t rows_per_batch, int nf, int nh, int nw,
+                      cudaStream_t st);
 void unpatchify_cfg(const float* head, int dtype, const int shape[4], const int patch[3], double w, void* eps,
                     cudaStream_t st);
 

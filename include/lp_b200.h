@@ -330,7 +330,8 @@ typedef struct lp_engine_config {
 
 typedef struct lp_engine lp_engine;
 
-/* NCCL plumbing for world > 1: rank 0 gets an id, the caller broadcasts it. */
+/* NCCL plumbing for world > 1: rank 0 gets an id, the caller broadcasts it.  With
+ * world == 1 a non-NULL id makes a 1-rank communicator and runs the same exchange path. */
 int lp_nccl_unique_id(uint8_t id_out[128]);
 int lp_engine_create(const lp_engine_config* cfg, const uint8_t* nccl_id, const double* cond, int32_t n_cond,
                      lp_engine** out);

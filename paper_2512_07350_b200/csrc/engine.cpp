@@ -122,7 +122,9 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
                 const int st = lp_dit_reserve_slots(c->dit, max_tokens, e->nslots);
                 if (st) fail(st, lp_last_error());
             }
-            if (c->world > 1) {
+            // world > 1 always exchanges through NCCL; world == 1 does when an id is given
+            // (a 1-rank communicator: exercises the exchange path on a single GPU)
+            if (c->world > 1 || nccl_id) {
                 if (!nccl_id) fail(LP_ERR_INVALID_ARGUMENT, "world > 1 needs an NCCL unique id");
                 ncclUniqueId id;
                 std::memcpy(&id, nccl_id, 128);
@@ -200,7 +202,7 @@ int lp_engine_run(lp_engine* e, int32_t first, int32_t count, void* stream) {
                     LP_CUDA(cudaStreamWaitEvent(st, e->ev_join[s], 0));
                 }
             }
-            if (c.world > 1) {
+            if (e->comm) {
                 const size_t slot = static_cast<size_t>(L.slot_elems) * E;
                 LP_NCCL(ncclAllGather(gather + slot * c.rank, gather, slot, ncclUint8, e->comm, st));
                 e->nccl_bytes += slot * static_cast<size_t>(c.world - 1);  // received by this rank

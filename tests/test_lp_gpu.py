@@ -145,3 +145,22 @@ def test_nonfinite_is_reported(cuda):
     lp.device_flags(reset=True)
     lp.cfg_predict(lp.IdentityDenoiser(), z, 1, [1.0] * 8, 3.0)  # f16 saturates, stays finite
     assert lp.device_flags() == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d", [2, 4])
+def test_engine_nccl_exchange_path_single_rank(cuda, oracle, d):
+    """The NCCL all-gather step of the engine (K9) on a 1-rank communicator: the same
+    ncclAllGather call and buffer layout as world > 1, bit-exact vs the oracle loop."""
+    dims = (16, 5, 16, 16)
+    z, cond = oracle.synthetic(dims, d, 2025)
+    want, ledger = oracle.run_lp(0, (1, 1, 1), z, d, 4, 0.05, 5.0, cond, (1, 2, 2), 2, 0.5)
+    eng = lp.LpEngine(dims, (1, 2, 2), d, 2, 0.5, 4, 0.05, 5.0, list(cond), denoiser="box", radius=(1, 1, 1),
+                      world=1, rank=0, nccl_id=lp.nccl_unique_id())
+    eng.load(lp.LatentTensor.from_numpy(z, d))
+    eng.run(1, 4)
+    got = lp.LatentTensor(eng.z.data.clone(), d).to_numpy()
+    comm = eng.comm()
+    eng.close()
+    assert np.array_equal(got, want)
+    assert comm["ledger_bytes"] == ledger and comm["nccl_bytes_received"] == 0

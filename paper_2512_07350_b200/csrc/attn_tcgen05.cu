@@ -248,6 +248,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             auto load_k = [&](int j) {
                 const int s = j % kKStages;
                 mbar_wait(&k_empty[s], ((j / kKStages) & 1) ^ 1);
+                if (POLY == -2 && j >= kKStages) {  // debug (attn_trace=3): no TMA once the ring is primed
+                    mbar_arrive(&k_full[s]);
+                    return;
+                }
                 mbar_arrive_expect_tx(&k_full[s], kTileBytes);
                 const int32_t kr = static_cast<int32_t>(b * a.kv_rows_per_batch + j * kTile);
                 tma_load_2d(&tk, &k_full[s], sK + s * kTileBytes, kc, kr);
@@ -256,6 +260,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             auto load_v = [&](int j) {
                 const int s = j % kVStages;
                 mbar_wait(&v_empty[s], ((j / kVStages) & 1) ^ 1);
+                if (POLY == -2 && j >= kVStages) {
+                    mbar_arrive(&v_full[s]);
+                    return;
+                }
                 mbar_arrive_expect_tx(&v_full[s], kTileBytes);
                 const int32_t kr = static_cast<int32_t>(b * a.kv_rows_per_batch + j * kTile);
                 tma_load_2d(&tv, &v_full[s], sV + s * kTileBytes, vc, kr);
@@ -338,7 +346,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             const int valid = static_cast<int>(a.n_kv - static_cast<int64_t>(j) * kTile);
             // the ragged last key block takes a separately compiled masked copy, so full
             // blocks carry no per-element compare/select
-            if (valid >= kTile)
+            if (POLY < 0) {  // debug (attn_trace=2/3): no softmax work, only the handoffs -> the MMA/sync floor
+                tc_fence_before();
+                mbar_arrive(&p_half[t]);
+                if (tr0) trace_ev<TR>(j, t, 2);
+                mbar_arrive(&p_full[t]);
+                if (tr0) trace_ev<TR>(j, t, 3);
+            } else if (valid >= kTile)
                 softmax_block<POLY, false, TR>(tS, tO, valid, c, m_run, l_run, &p_half[t], &p_full[t], j, t, tr0);
             else
                 softmax_block<POLY, true, TR>(tS, tO, valid, c, m_run, l_run, &p_half[t], &p_full[t], j, t, tr0);
@@ -383,6 +397,8 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
         LP_CUDA(cudaFuncSetAttribute(k_attention<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         LP_CUDA(cudaFuncSetAttribute(k_attention<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         LP_CUDA(cudaFuncSetAttribute(k_attention<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention<-1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention<-2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         attr = true;
     }
     if ((x.ldq | x.ldk | x.ldv | x.ldo) % 8) fail(LP_ERR_INVALID_ARGUMENT, "attention: strides must be multiples of 8");
@@ -404,8 +420,10 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     const dim3 grid(static_cast<unsigned>((x.n_q + 2 * kTile - 1) / (2 * kTile)), x.heads, x.batch);
     const int cls = x.n_kv == x.n_q && x.q == x.k ? KC_SELF_ATTN : KC_CROSS_ATTN;
     prof_begin(cls, st);
-    switch (tune_get("attn_trace", 0) ? -1 : attn_poly()) {
+    switch (tune_get("attn_trace", 0) ? -tune_get("attn_trace", 0) : attn_poly()) {
         case -1: k_attention<0, true><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
+        case -2: k_attention<-1, true><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
+        case -3: k_attention<-2, true><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
         case 0: k_attention<0><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
         case 6: k_attention<6><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
         default: k_attention<4><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;

@@ -1,6 +1,6 @@
 """Timeline of one attention CTA (clock64 stamps from the TR kernel variant).
 
-usage: python scripts/attn_trace.py [S]
+usage: python scripts/attn_trace.py [S] [mode: 1 = real kernel, 2 = no softmax work (MMA/sync floor)]
 Prints, per key block j and Q tile t, cycle offsets of: S ready, max done, p_half,
 p_full (softmax side) and MMA-warp wakeups, plus the steady-state per-block period."""
 import ctypes as C
@@ -17,7 +17,7 @@ S = int(sys.argv[1]) if len(sys.argv) > 1 else 18720
 q, k, v, o = (torch.randn(2, S, 12, 128, device="cuda").bfloat16() for _ in range(4))
 buf = torch.zeros(64 * 2 * 8, dtype=torch.int64, device="cuda")
 _lib.check(L.lp_attention_set_trace(C.c_void_p(buf.data_ptr())))
-_lib.check(L.lp_tune(b"attn_trace", 1))
+_lib.check(L.lp_tune(b"attn_trace", int(sys.argv[2]) if len(sys.argv) > 2 else 1))
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 for _ in range(3):
     _lib.check(L.lp_attention_bf16(C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()), C.c_void_p(v.data_ptr()),

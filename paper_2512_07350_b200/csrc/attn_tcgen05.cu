@@ -277,55 +277,75 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        // The whole warp runs the issue loop (converged: the barrier checks are warp-wide and
+        // the operands stay in uniform registers); one elected lane issues the MMAs and
+        // commits.  tcgen05.mma issue is nearly synchronous with execution, so each check in
+        // this loop is a pipe bubble: ~38 cycles converged vs ~106 from a lone divergent lane
+        // (scripts/micro/mma_bench.py, profiles/r1n).
+        const bool leader = elect_one();
+        // warp-wide waits that suspend in hardware (try_wait with a time hint) instead of
+        // spinning: 32 spinning lanes would steal issue slots from the softmax warps sharing
+        // this SMSP
+        auto wait1 = [&](uint64_t* bar, uint32_t parity) { mbar_wait_sleep(bar, parity); };
+        {
             constexpr uint32_t idS = idesc_bf16(128, 128);
             constexpr uint32_t idO = idesc_bf16(128, 128, /*b_mn_major=*/true);
             // descriptors built once; per-k offsets go into the start-address field (addr >> 4)
             const uint64_t dQ = desc_sw128(smem_u32(sQ)), dK = desc_sw128(smem_u32(sK));
             const uint64_t dV = desc_sw128(smem_u32(sV), /*sbo=*/1024, /*lbo=*/kAtom);
-            mbar_wait(q_full, 0);
+            wait1(q_full, 0);
             auto issue_s = [&](int t, int j) {
                 const int s = j % kKStages;
                 if (t == 0) {
-                    mbar_wait(&k_full[s], (j / kKStages) & 1);
+                    wait1(&k_full[s], (j / kKStages) & 1);
                     tc_fence_after();
                 }
-                const uint64_t q0 = dQ + t * (kTileBytes >> 4), k0 = dK + s * (kTileBytes >> 4);
+                if (leader) {
+                    const uint64_t q0 = dQ + t * (kTileBytes >> 4), k0 = dK + s * (kTileBytes >> 4);
 #pragma unroll
-                for (int k = 0; k < kHD / 16; ++k) {
-                    const uint64_t off = static_cast<uint64_t>((k >> 2) * kAtom + (k & 3) * 32) >> 4;
-                    mma_ss(tmem + t * 128, q0 + off, k0 + off, idS, k != 0);
+                    for (int k = 0; k < kHD / 16; ++k) {
+                        const uint64_t off = static_cast<uint64_t>((k >> 2) * kAtom + (k & 3) * 32) >> 4;
+                        mma_ss(tmem + t * 128, q0 + off, k0 + off, idS, k != 0);
+                    }
+                    mma_commit(&s_full[t]);
+                    if (t == 1) mma_commit(&k_empty[s]);  // both tiles' S issued: K_j slot frees on completion
                 }
-                mma_commit(&s_full[t]);
-                if (t == 1) mma_commit(&k_empty[s]);  // both tiles' S issued: K_j slot frees on completion
+                __syncwarp();
             };
             auto issue_pv = [&](int t, int j, int half) {
-                const uint64_t v0 = dV + (j % kVStages) * (kTileBytes >> 4);
+                if (leader) {
+                    const uint64_t v0 = dV + (j % kVStages) * (kTileBytes >> 4);
 #pragma unroll
-                for (int k = half * 4; k < half * 4 + 4; ++k) {
-                    // A = P_t (TMEM, bf16 pairs: 8 columns per 16 kv); B = V [kv][d] MN-major:
-                    // 16 kv rows per step (2048 B), d halves LBO = 16 KB apart
-                    mma_ts(tmem + 256 + t * 128, tmem + t * 128 + k * 8, v0 + ((k * 2048) >> 4), idO, (j | k) != 0);
+                    for (int k = half * 4; k < half * 4 + 4; ++k) {
+                        // A = P_t (TMEM, bf16 pairs: 8 columns per 16 kv); B = V [kv][d] MN-major:
+                        // 16 kv rows per step (2048 B), d halves LBO = 16 KB apart
+                        mma_ts(tmem + 256 + t * 128, tmem + t * 128 + k * 8, v0 + ((k * 2048) >> 4), idO,
+                               (j | k) != 0);
+                    }
                 }
+                __syncwarp();
             };
             issue_s(0, 0);
             issue_s(1, 0);
             for (int j = 0; j < nkv; ++j) {
                 const bool more = j + 1 < nkv;
                 for (int t = 0; t < 2; ++t) {
-                    mbar_wait(&p_half[t], j & 1);
-                    if (t == 0) mbar_wait(&v_full[j % kVStages], (j / kVStages) & 1);
-                    trace_ev<TR>(j, t, 4);
+                    wait1(&p_half[t], j & 1);
+                    if (t == 0) wait1(&v_full[j % kVStages], (j / kVStages) & 1);
+                    if (lane == 0) trace_ev<TR>(j, t, 4);
                     tc_fence_after();
                     issue_pv(t, j, 0);
-                    mbar_wait(&p_full[t], j & 1);
-                    trace_ev<TR>(j, t, 5);
+                    wait1(&p_full[t], j & 1);
+                    if (lane == 0) trace_ev<TR>(j, t, 5);
                     tc_fence_after();
                     issue_pv(t, j, 1);
-                    if (!more) mma_commit(&o_final[t]);
-                    if (t == 1) mma_commit(&v_empty[j % kVStages]);
+                    if (leader) {
+                        if (!more) mma_commit(&o_final[t]);
+                        if (t == 1) mma_commit(&v_empty[j % kVStages]);
+                    }
+                    __syncwarp();
                     if (more) issue_s(t, j + 1);
-                    trace_ev<TR>(j, t, 6);
+                    if (lane == 0) trace_ev<TR>(j, t, 6);
                 }
             }
         }
@@ -385,8 +405,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 }
 
 static int attn_poly() {
-    // pairs out of every 16 whose exp2 runs on the FMA pipe (0, 4, 6 compiled)
-    const int v = tune_get("attn_poly", 4);
+    // pairs out of every 16 whose exp2 runs on the FMA pipe (0, 4, 6 compiled; A/B r1n: 6 best)
+    const int v = tune_get("attn_poly", 6);
     return v == 0 || v == 6 ? v : 4;
 }
 

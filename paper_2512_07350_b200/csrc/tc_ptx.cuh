@@ -66,6 +66,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         if ((++n & 1023) == 0 && clock64() - t0 > (1ll << 35)) __trap();
     }
 }
+// Same, but each try_wait may suspend the thread in hardware (up to ~1 us per try) until the
+// phase completes, instead of returning immediately: waiting warps stop consuming issue slots.
+__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t a, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity), "r"(1000u)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    if (mbar_try_wait_hint(a, parity)) return;
+    const long long t0 = clock64();
+    uint32_t n = 0;
+    while (!mbar_try_wait_hint(a, parity)) {
+        if ((++n & 1023) == 0 && clock64() - t0 > (1ll << 35)) __trap();
+    }
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

@@ -186,29 +186,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_bf16(kBM, BN);
-            int s = 0;
-            uint32_t ph = 0;
-            int it = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-                const int acc = it & 1;
-                const uint32_t aph = (it >> 1) & 1;
-                mbar_wait(&tempty[acc], aph ^ 1);
+        // converged MMA-issue warp, one elected lane issues (see k_gemm2)
+        const bool leader = elect_one();
+        constexpr uint32_t idesc = idesc_bf16(kBM, BN);
+        const uint64_t dA = desc_sw128(smem_u32(sA)), dB = desc_sw128(smem_u32(sB));
+        int s = 0;
+        uint32_t ph = 0;
+        int it = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+            const int acc = it & 1;
+            const uint32_t aph = (it >> 1) & 1;
+            mbar_wait(&tempty[acc], aph ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem + acc * BN;
+            for (int kb = 0; kb < nk; ++kb) {
+                mbar_wait(&full[s], ph);
                 tc_fence_after();
-                const uint32_t d = tmem + acc * BN;
-                for (int kb = 0; kb < nk; ++kb) {
-                    mbar_wait(&full[s], ph);
-                    tc_fence_after();
-                    const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+                if (leader) {
+                    const uint64_t a0 = dA + static_cast<uint64_t>(s * A_BYTES >> 4);
+                    const uint64_t b0 = dB + static_cast<uint64_t>(s * B_BYTES >> 4);
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k)
-                        mma_ss(d, desc_sw128(a0 + k * 32), desc_sw128(b0 + k * 32), idesc, (kb | k) != 0);
+                    for (int k = 0; k < kBK / 16; ++k) mma_ss(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);
                     mma_commit(&empty[s]);
-                    if (++s == kStages) { s = 0; ph ^= 1; }
                 }
-                mma_commit(&tfull[acc]);
+                __syncwarp();
+                if (++s == kStages) { s = 0; ph ^= 1; }
             }
+            if (leader) mma_commit(&tfull[acc]);
+            __syncwarp();
         }
     } else {
         // epilogue: warps 2..5 -> TMEM lane quadrant warp % 4
@@ -308,8 +313,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {
+        // MMA issuer (leader CTA): the whole warp runs the loop converged — barrier checks are
+        // warp-wide, descriptors stay in uniform registers — and one elected lane issues.
+        // tcgen05.mma issue is nearly synchronous with execution, so a check from a lone
+        // divergent lane costs ~100 pipe cycles per k-block (scripts/micro/mma_bench.py).
+        if (rank == 0) {
+            const bool leader = elect_one();
             constexpr uint32_t idesc = idesc_bf16(2 * kBM, BN);
+            const uint64_t dA = desc_sw128(smem_u32(sA)), dB = desc_sw128(smem_u32(sB));
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
@@ -322,14 +333,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
-                    const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+                    if (leader) {
+                        const uint64_t a0 = dA + static_cast<uint64_t>(s * A_BYTES >> 4);
+                        const uint64_t b0 = dB + static_cast<uint64_t>(s * B_BYTES >> 4);
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k)
-                        mma_ss_2sm(d, desc_sw128(a0 + k * 32), desc_sw128(b0 + k * 32), idesc, (kb | k) != 0);
-                    mma_commit_2sm(&empty[s], 0x3);
+                        for (int k = 0; k < kBK / 16; ++k)
+                            mma_ss_2sm(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);  // +32 B per K=16
+                        mma_commit_2sm(&empty[s], 0x3);
+                    }
+                    __syncwarp();
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
-                mma_commit_2sm(&tfull[acc], 0x3);
+                if (leader) mma_commit_2sm(&tfull[acc], 0x3);
+                __syncwarp();
             }
         }
     } else {

@@ -52,7 +52,8 @@ def _cmd(src, extra):
                            "-o", obj]
     lang = ["-x", "cu"]  # .cpp too: they share the device codec header
     cmd = [NVCC, *lang, "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-           "--expt-relaxed-constexpr", *INCS, *extra, "-c", path, "-o", obj]
+           "--expt-relaxed-constexpr", *INCS, *extra, *os.environ.get("LP_NVCC_EXTRA", "").split(), "-c", path,
+           "-o", obj]
     return path, obj, cmd
 
 

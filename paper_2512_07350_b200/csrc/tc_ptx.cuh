@@ -57,14 +57,24 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // a protocol bug surfaces as a launch error instead of a hung GPU.  clock64 (CS2R) is
 // cheap; %globaltimer reads on every missed first try cost hundreds of cycles on the
 // critical MMA-issue path (r1g attention timeline).
+__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t a, uint32_t parity);
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
+#ifdef LP_MBAR_SLEEP
+    if (mbar_try_wait_hint(a, parity)) return;
+    const long long t0 = clock64();
+    uint32_t n = 0;
+    while (!mbar_try_wait_hint(a, parity)) {
+        if ((++n & 1023) == 0 && clock64() - t0 > (1ll << 35)) __trap();
+    }
+#else
     if (mbar_try_wait(a, parity)) return;
     const long long t0 = clock64();
     uint32_t n = 0;
     while (!mbar_try_wait(a, parity)) {
         if ((++n & 1023) == 0 && clock64() - t0 > (1ll << 35)) __trap();
     }
+#endif
 }
 // Same, but each try_wait may suspend the thread in hardware (up to ~1 us per try) until the
 // phase completes, instead of returning immediately: waiting warps stop consuming issue slots.

@@ -152,13 +152,50 @@ def reference_dit_step(ref, dit, z, cond, K, flop_scale):
     return (wall - dit_wall) + dit_wall * flop_scale, wall, dit_wall
 
 
-def run_reference_arm(args, rank, world):
-    if rank != 0:
-        return
+def reference_dit_baseline(K, threads, samples, warmup):
+    """The reference's CPU path on the metric's workload: the UNMODIFIED reference run_lp
+    (oracle/_ref) with the fp32 CPU WAN-1.3B DiT in its Denoiser slot (oracle/cpu_dit.py),
+    `samples` bounded samples (see reference_dit_step).  Returns (steps/s, sample text)."""
     import torch
 
     from oracle.cpu_dit import CpuDiT, dit_flops
-    from oracle.oracle import Reference, reference_available
+    from oracle.oracle import Reference, sub_shape
+
+    os.environ["LPSIM_THREADS"] = str(threads)
+    workers = min(threads, K)
+    torch.set_num_threads(max(1, threads // workers))
+    ref = Reference()
+    z, cond = ref.synthetic(DIMS, 4, SEED)
+    dit = CpuDiT(num_layers=1)
+
+    def axis_flops(step):  # the reference's own plans
+        p = ref.build_plan(DIMS, PATCH, step, K, R_OVERLAP)
+        return sum(dit_flops(sub_shape(DIMS, p, k), PATCH) for k in range(p.n))
+
+    cycle = sum(axis_flops(s) for s in (1, 2, 3)) / 3
+    scale = 30 * cycle / axis_flops(1)   # run_lp's single sampled step is step 1 (T axis)
+    for _ in range(warmup):
+        reference_dit_step(ref, dit, z, cond, K, scale)
+    est, walls, dits = [], [], []
+    for _ in range(samples):
+        e, w, dw = reference_dit_step(ref, dit, z, cond, K, scale)
+        est.append(e)
+        walls.append(w)
+        dits.append(dw)
+    value = len(est) / sum(est)
+    sample = (f"UNMODIFIED reference run_lp (oracle/_ref) for 1 step (T axis) of C2 (16x21x60x104 f32, K={K}, "
+              f"r={R_OVERLAP}, eta {ETA}, w {W_CFG}) with an fp32 torch CPU WAN-1.3B-shaped DiT (1 of 30 blocks, "
+              f"random weights) in its Denoiser slot; {samples} sample(s): measured wall {statistics.mean(walls):.2f} s "
+              f"of which DiT {statistics.mean(dits):.2f} s, DiT part scaled x{scale:.2f} (30 blocks x cycle-mean/T-axis "
+              f"shard FLOPs); LPSIM_THREADS={threads}, {workers} workers x {torch.get_num_threads()} torch threads; "
+              f"{warmup} warm-up sample(s)")
+    return value, sample
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    from oracle.oracle import reference_available
 
     K = args.workers or max(4, world)
     threads = os.cpu_count() or 1
@@ -169,35 +206,7 @@ def run_reference_arm(args, rank, world):
     cpu_reference_run(1, K, threads)
     lp_only, lp_info = cpu_reference_run(args.steps, K, threads)
     # the metric's workload: reference run_lp + a WAN-1.3B-shaped fp32 DiT in the Denoiser slot
-    os.environ["LPSIM_THREADS"] = str(threads)
-    workers = min(threads, K)
-    torch.set_num_threads(max(1, threads // workers))
-    ref = Reference()
-    z, cond = ref.synthetic(DIMS, 4, SEED)
-    dit = CpuDiT(num_layers=1)
-    from oracle.oracle import sub_shape
-
-    def axis_flops(step):  # the reference's own plans
-        p = ref.build_plan(DIMS, PATCH, step, K, R_OVERLAP)
-        return sum(dit_flops(sub_shape(DIMS, p, k), PATCH) for k in range(p.n))
-
-    cycle = sum(axis_flops(s) for s in (1, 2, 3)) / 3
-    scale = 30 * cycle / axis_flops(1)   # run_lp's single sampled step is step 1 (T axis)
-    for _ in range(min(args.warmup, 1)):
-        reference_dit_step(ref, dit, z, cond, K, scale)
-    est, walls, dits = [], [], []
-    for _ in range(args.steps):
-        e, w, dw = reference_dit_step(ref, dit, z, cond, K, scale)
-        est.append(e)
-        walls.append(w)
-        dits.append(dw)
-    value = len(est) / sum(est)
-    sample = (f"UNMODIFIED reference run_lp (oracle/_ref) for 1 step (T axis) of C2 (16x21x60x104 f32, K={K}, "
-              f"r={R_OVERLAP}, eta {ETA}, w {W_CFG}) with an fp32 torch CPU WAN-1.3B-shaped DiT (1 of 30 blocks, "
-              f"random weights) in its Denoiser slot; per sample: measured wall {statistics.mean(walls):.2f} s of which "
-              f"DiT {statistics.mean(dits):.2f} s, DiT part scaled x{scale:.2f} (30 blocks x cycle-mean/T-axis shard "
-              f"FLOPs); LPSIM_THREADS={threads}, {workers} workers x {torch.get_num_threads()} torch threads; "
-              f"{min(args.warmup, 1)} warm-up sample")
+    value, sample = reference_dit_baseline(K, threads, args.steps, min(args.warmup, 1))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
@@ -268,8 +277,8 @@ def run_ours(args, rank, world, local_rank):
     launches = int(L.lp_launch_count() - l0)
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     c1 = eng.comm()
-    nl = (C.c_uint64 * 3)()
-    kms, kfl, kby = (C.c_double * 3)(), (C.c_double * 3)(), (C.c_double * 3)()
+    nl = (C.c_uint64 * 6)()
+    kms, kfl, kby = (C.c_double * 6)(), (C.c_double * 6)(), (C.c_double * 6)()
 
     # ---- end-to-end through the C-ABI engine with host buffers ----
     zin = torch.empty(DIMS, dtype=torch.float32).pin_memory()
@@ -311,6 +320,25 @@ def run_ours(args, rank, world, local_rank):
     names = ["self_attention", "cross_attention", "gemm"]
     kern = {names[i]: {"launches": int(nl[i]), "ms": kms[i], "tflops": (kfl[i] / kms[i] / 1e9) if kms[i] else None,
                        "share_of_step": kms[i] / prof_ms if prof_ms else None} for i in range(3)}
+    peaks_hbm = None
+    try:
+        peaks_hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
+    except Exception:
+        pass
+    peaks_hbm = peaks_hbm or 7700.0
+    hbm = {}
+    for i, nm in ((4, "k1_gather"), (5, "k10_reconstruct_update")):
+        gbps = kby[i] / kms[i] / 1e6 if kms[i] else None
+        hbm[nm] = {"launches": int(nl[i]), "ms": kms[i], "algorithmic_bytes": kby[i], "GBps": gbps,
+                   "frac_of_hbm": gbps / peaks_hbm if gbps else None, "share_of_step": kms[i] / prof_ms if prof_ms else None}
+    hbm["peak_GBps"] = peaks_hbm
+    hbm["peak_source"] = "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"
+    ag = None
+    if world > 1:
+        ag_gbps = kby[3] / kms[3] / 1e6 if kms[3] else None
+        ag = {"launches": int(nl[3]), "ms": kms[3], "bytes_received_per_rank": kby[3], "GBps_per_rank": ag_gbps,
+              "nvlink_peak_GBps_per_direction": 900.0, "frac": ag_gbps / 900.0 if ag_gbps else None,
+              "share_of_step": kms[3] / prof_ms if prof_ms else None}
     dom = max(range(3), key=lambda i: kms[i])
     peaks = {}
     try:
@@ -356,15 +384,25 @@ def run_ours(args, rank, world, local_rank):
                      "step": {"algorithmic_tflop_per_step_per_rank": step_flops / 1e12, "achieved": step_tflops,
                               "frac": step_tflops / peak}},
         "kernels": kern,
+        "hbm_kernels": hbm,
+        "allgather": ag,
         "clocks": clk.summary(),
         "comm": {"nccl_bytes_per_step_measured_all_ranks": per_step_nccl,
                  "allgather_bytes_per_video": ag, "reference_ledger_bytes_per_video": led,
                  "reference_nmp_bytes_per_video": nmp, "wire": "f32 eps shards (ledger counts the 2-B preset width)"},
     }
     if world == 1 and not args.no_cpu_baseline:
-        v, info = cpu_reference_run(args.cpu_steps, K, os.cpu_count() or 1)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
-                                "sample": info["sample"]}
+        from oracle.oracle import reference_available
+
+        threads = os.cpu_count() or 1
+        v_lp, info = cpu_reference_run(args.cpu_steps, K, threads)
+        line["cpu_baseline_lp_machinery_only"] = {"value": v_lp, "unit": UNIT, "cores": info["cores"],
+                                                  "kind": info["kind"], "sample": info["sample"]}
+        if reference_available():
+            v, sample = reference_dit_baseline(K, threads, 1, 0)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample}
+        else:
+            line["cpu_baseline"] = dict(line["cpu_baseline_lp_machinery_only"])
     print(json.dumps(line), flush=True)
     eng.close()
 

@@ -197,8 +197,9 @@ int lp_device_flags(uint32_t* flags_out, int reset);
 /* Kernel launches issued by this library since load. */
 uint64_t lp_launch_count(void);
 /* Live per-kernel-class timing with CUDA events on the launching stream
- * (classes: 0 self-attention, 1 cross-attention, 2 GEMM).  collect() fills 3
- * entries each: launches, device ms, algorithmic FLOPs, algorithmic bytes. */
+ * (classes: 0 self-attention, 1 cross-attention, 2 GEMM, 3 K9 all-gather, 4 K1 gather,
+ * 5 K10 reconstruct+update).  collect() fills 6 entries each: launches, device ms,
+ * algorithmic FLOPs, algorithmic bytes. */
 int lp_profile_enable(int on);
 /* Kernel-variant knobs (benchmarking): "attn_poly" (0-3: eighths of exp2 on the
  * FMA pipe), "gemm_2sm" (0/1: CTA-pair GEMM).  Also read from LP_TUNE_<KEY>. */

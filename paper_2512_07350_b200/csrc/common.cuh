@@ -66,7 +66,13 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 // Optional per-kernel-class timing (CUDA events on the launching stream), used by
 // bench.py to measure the dominant kernel's live duration inside the timed region.
-enum KernelClass { KC_SELF_ATTN = 0, KC_CROSS_ATTN = 1, KC_GEMM = 2, KC_COUNT = 3 };
+enum KernelClass {
+    KC_SELF_ATTN = 0, KC_CROSS_ATTN = 1, KC_GEMM = 2,
+    KC_ALLGATHER = 3,  // K9 ncclAllGather (bytes = received by this rank)
+    KC_GATHER = 4,     // K1 partition gather (bytes = read + write)
+    KC_RECON = 5,      // K10 reconstruct + sampler update (bytes = shards + z read, z write)
+    KC_COUNT = 6
+};
 bool prof_enabled();
 void prof_begin(int cls, cudaStream_t st);
 void prof_end(int cls, cudaStream_t st, double flops, double bytes);

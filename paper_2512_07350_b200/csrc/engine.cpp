@@ -204,7 +204,9 @@ int lp_engine_run(lp_engine* e, int32_t first, int32_t count, void* stream) {
             }
             if (e->comm) {
                 const size_t slot = static_cast<size_t>(L.slot_elems) * E;
+                prof_begin(KC_ALLGATHER, st);
                 LP_NCCL(ncclAllGather(gather + slot * c.rank, gather, slot, ncclUint8, e->comm, st));
+                prof_end(KC_ALLGATHER, st, 0.0, static_cast<double>(slot) * (c.world - 1));
                 e->nccl_bytes += slot * static_cast<size_t>(c.world - 1);  // received by this rank
             }
             reconstruct_dispatch(e->recon[a], E, gather, e->z, nullptr, true, c.mode == LP_MODE_FAST, st);  // K10

@@ -63,12 +63,43 @@ __global__ void __launch_bounds__(256) k_slice_copy(const V* __restrict__ src, V
     }
 }
 
+// 32-bit variant (outer*run < 2^31): row/offset split by multiply-shift division, 4
+// independent vectors in flight per thread per iteration.
+template <typename V>
+__global__ void __launch_bounds__(256) k_slice_copy32(const V* __restrict__ src, V* __restrict__ dst, uint32_t total,
+                                                      uint32_t run, FastDiv div_run, uint32_t src_stride,
+                                                      uint32_t src_off) {
+    const uint32_t step = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < total; base += 4 * step) {
+        V v[4];
+        uint32_t at[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t idx = base + u * step;
+            at[u] = idx;
+            if (idx < total) {
+                const uint32_t o = static_cast<uint32_t>((static_cast<uint64_t>(idx) * div_run.mul) >> div_run.shift);
+                v[u] = __ldg(src + static_cast<uint64_t>(o) * src_stride + src_off + (idx - o * run));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (at[u] < total) dst[at[u]] = v[u];
+    }
+}
+
 template <typename V>
 static void launch_slice(const void* src, void* dst, int64_t outer, int64_t run, int64_t stride, int64_t off,
                          cudaStream_t st) {
     const int64_t total = outer * run;
-    k_slice_copy<V><<<grid_for(total, 256), 256, 0, st>>>(static_cast<const V*>(src), static_cast<V*>(dst), outer, run,
-                                                          stride, off);
+    if (total < (1ll << 31) && outer * stride < (1ll << 32)) {
+        k_slice_copy32<V><<<grid_for((total + 3) / 4, 256, 16), 256, 0, st>>>(
+            static_cast<const V*>(src), static_cast<V*>(dst), static_cast<uint32_t>(total), static_cast<uint32_t>(run),
+            make_fastdiv(static_cast<uint32_t>(run)), static_cast<uint32_t>(stride), static_cast<uint32_t>(off));
+    } else {
+        k_slice_copy<V><<<grid_for(total, 256), 256, 0, st>>>(static_cast<const V*>(src), static_cast<V*>(dst), outer,
+                                                              run, stride, off);
+    }
     LP_LAUNCH_CHECK();
 }
 
@@ -78,16 +109,19 @@ void slice_to(const void* z, const Shape4& s, int axis, i64 begin, i64 end, int 
     const i64 D = s.extent(axis);
     const i64 run_b = (end - begin) * inner * E, stride_b = D * inner * E, off_b = begin * inner * E;
     const uintptr_t al = reinterpret_cast<uintptr_t>(z) | reinterpret_cast<uintptr_t>(dst);
+    prof_begin(KC_GATHER, st);
     for (int vb : {16, 8, 4, 2, 1}) {
         if (run_b % vb || stride_b % vb || off_b % vb || al % vb) continue;
         switch (vb) {
-            case 16: launch_slice<uint4>(z, dst, outer, run_b / 16, stride_b / 16, off_b / 16, st); return;
-            case 8: launch_slice<uint2>(z, dst, outer, run_b / 8, stride_b / 8, off_b / 8, st); return;
-            case 4: launch_slice<uint32_t>(z, dst, outer, run_b / 4, stride_b / 4, off_b / 4, st); return;
-            case 2: launch_slice<uint16_t>(z, dst, outer, run_b / 2, stride_b / 2, off_b / 2, st); return;
-            default: launch_slice<uint8_t>(z, dst, outer, run_b, stride_b, off_b, st); return;
+            case 16: launch_slice<uint4>(z, dst, outer, run_b / 16, stride_b / 16, off_b / 16, st); break;
+            case 8: launch_slice<uint2>(z, dst, outer, run_b / 8, stride_b / 8, off_b / 8, st); break;
+            case 4: launch_slice<uint32_t>(z, dst, outer, run_b / 4, stride_b / 4, off_b / 4, st); break;
+            case 2: launch_slice<uint16_t>(z, dst, outer, run_b / 2, stride_b / 2, off_b / 2, st); break;
+            default: launch_slice<uint8_t>(z, dst, outer, run_b, stride_b, off_b, st); break;
         }
+        break;
     }
+    prof_end(KC_GATHER, st, 0.0, 2.0 * static_cast<double>(outer) * static_cast<double>(run_b));
 }
 
 // ---------------------------------------------------------------------------
@@ -262,15 +296,82 @@ __global__ void __launch_bounds__(256) k_reconstruct(const __grid_constant__ Rec
     }
 }
 
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
+    return static_cast<uint32_t>((static_cast<uint64_t>(x) * f.mul) >> f.shift);
+}
+
+// K10, exact mode, 32-bit indexing: the per-position weights w_k(x) and their sum
+// Z(x) = Σ_k w_k(x) (worker order, the same IEEE divisions and adds as entry_weight and
+// the reference) are tabulated once per block in shared memory ([n+1][D] doubles); every
+// element then costs its shard loads, Σ w·pred in worker order, one true division and
+// the sampler update.  Index decomposition uses multiply-shift division (FastDiv).
+template <int D, bool UPDATE>
+__global__ void __launch_bounds__(256) k_reconstruct_tab(const __grid_constant__ ReconParams p,
+                                                         const typename Store<D>::T* __restrict__ preds,
+                                                         typename Store<D>::T* __restrict__ z,
+                                                         typename Store<D>::T* __restrict__ eps_out) {
+    extern __shared__ double wt[];  // [n][Dx] weights, then [Dx] sums
+    const int Dx = static_cast<int>(p.D), n = p.n;
+    double* zsum = wt + n * Dx;
+    for (int x = threadIdx.x; x < Dx; x += blockDim.x) {
+        double zs = 0.0;
+        for (int k = 0; k < n; ++k) {
+            const ReconEntry& e = p.e[k];
+            const int64_t j = x - e.begin;
+            const double w = (j < 0 || j >= e.len) ? 0.0 : entry_weight(e, j);
+            if (j >= 0 && j < e.len) zs = __dadd_rn(zs, w);
+            wt[k * Dx + x] = w;
+        }
+        zsum[x] = zs;
+    }
+    __syncthreads();
+    const uint32_t total = static_cast<uint32_t>(p.total), inner = static_cast<uint32_t>(p.inner);
+    for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const uint32_t ox = fdiv(idx, p.div_inner);
+        const uint32_t i = idx - ox * inner;
+        const uint32_t o = fdiv(ox, p.div_d);
+        const int x = static_cast<int>(ox - o * static_cast<uint32_t>(Dx));
+        double a = 0.0;
+        for (int k = 0; k < n; ++k) {
+            const ReconEntry& e = p.e[k];
+            const int64_t j = x - e.begin;
+            if (j < 0) break;  // entries are sorted by begin
+            if (j >= e.len) continue;
+            const double w = wt[k * Dx + x];
+            if (w != 0.0)
+                a = __dadd_rn(a, __dmul_rn(w, load_val<D>(preds, e.base + (static_cast<int64_t>(o) * e.len + j) * inner + i)));
+        }
+        const double eps = quantize_dev<D>(__ddiv_rn(a, zsum[x]));
+        bool ok = isfinite(eps);
+        if (UPDATE) ok = store_q<D>(z, idx, __dsub_rn(load_val<D>(z, idx), __dmul_rn(p.eta, eps))) && ok;
+        else ok = store_q<D>(eps_out, idx, eps) && ok;
+        if (!ok) raise_flag(LP_FLAG_NONFINITE);
+    }
+}
+
 template <int D, bool UPDATE>
 static void launch_recon(const ReconParams& p, const void* preds, void* z, void* eps, bool fast, cudaStream_t st) {
     using T = typename Store<D>::T;
     const int g = grid_for(p.total, 256);
-    if (fast)
+    const size_t tab = sizeof(double) * static_cast<size_t>(p.n + 1) * static_cast<size_t>(p.D);
+    if (!fast && p.use32 && tab <= 48 * 1024) {
+        k_reconstruct_tab<D, UPDATE><<<g, 256, tab, st>>>(p, static_cast<const T*>(preds), static_cast<T*>(z),
+                                                          static_cast<T*>(eps));
+    } else if (fast)
         k_reconstruct<D, UPDATE, true><<<g, 256, 0, st>>>(p, static_cast<const T*>(preds), static_cast<T*>(z), static_cast<T*>(eps));
     else
         k_reconstruct<D, UPDATE, false><<<g, 256, 0, st>>>(p, static_cast<const T*>(preds), static_cast<T*>(z), static_cast<T*>(eps));
     LP_LAUNCH_CHECK();
+}
+
+FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    f.shift = 31 + l;
+    f.mul = ((1ull << f.shift) + d - 1) / d;
+    return f;
 }
 
 ReconParams make_recon_params(const lp_plan& plan, const Shape4& s, const std::vector<i64>& base, double eta) {
@@ -286,6 +387,11 @@ ReconParams make_recon_params(const lp_plan& plan, const Shape4& s, const std::v
     p.D = plan.axis_extent;
     p.total = s.volume();
     p.eta = eta;
+    p.use32 = p.total < (1ll << 31) ? 1 : 0;
+    if (p.use32) {
+        p.div_inner = make_fastdiv(static_cast<uint32_t>(p.inner));
+        p.div_d = make_fastdiv(static_cast<uint32_t>(p.D));
+    }
     for (int k = 0; k < plan.n_entries; ++k) {
         const lp_entry& e = plan.entries[k];
         p.e[k] = ReconEntry{e.latent_begin, e.latent_end - e.latent_begin, e.delta_start, e.delta_end, base[k]};
@@ -295,12 +401,18 @@ ReconParams make_recon_params(const lp_plan& plan, const Shape4& s, const std::v
 
 void reconstruct_dispatch(const ReconParams& p, int dtype, const void* preds, void* z, void* eps, bool update,
                           bool fast, cudaStream_t st) {
+    // algorithmic bytes: every shard element read once, z read (update) and the result written
+    double shard = 0.0;
+    for (int k = 0; k < p.n; ++k) shard += static_cast<double>(p.e[k].len);
+    const double per_pos = static_cast<double>(p.total) / static_cast<double>(p.D);
+    prof_begin(KC_RECON, st);
     switch (dtype) {
         case 2: update ? launch_recon<2, true>(p, preds, z, eps, fast, st) : launch_recon<2, false>(p, preds, z, eps, fast, st); break;
         case 4: update ? launch_recon<4, true>(p, preds, z, eps, fast, st) : launch_recon<4, false>(p, preds, z, eps, fast, st); break;
         case 8: update ? launch_recon<8, true>(p, preds, z, eps, fast, st) : launch_recon<8, false>(p, preds, z, eps, fast, st); break;
         default: fail(LP_ERR_INVALID_ARGUMENT, "bad dtype");
     }
+    prof_end(KC_RECON, st, 0.0, (shard * per_pos + (update ? 2.0 : 1.0) * static_cast<double>(p.total)) * dtype);
 }
 
 template <int D>

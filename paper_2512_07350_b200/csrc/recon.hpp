@@ -12,10 +12,21 @@ constexpr int kMaxKernelEntries = 64;
 struct ReconEntry {
     int64_t begin, len, ds, de, base;
 };
+// Division by a runtime-constant divisor d < 2^31 for dividends x < 2^31:
+// q = (x * mul) >> shift with mul = ceil(2^(31+l) / d), l = ceil(log2 d), shift = 31 + l
+// (Granlund–Montgomery: exact for every x < 2^31; mul < 2^32 + 1 fits in 64 bits).
+struct FastDiv {
+    uint64_t mul = 1;
+    uint32_t shift = 0, d = 1;
+};
+FastDiv make_fastdiv(uint32_t d);
+
 struct ReconParams {
     int n;
     int64_t D, outer, inner, total;
     double eta;
+    FastDiv div_inner, div_d;  // valid (use32) when total < 2^31
+    int use32;
     ReconEntry e[kMaxKernelEntries];
 };
 

@@ -8,11 +8,13 @@
 // worker-ordered sums, true division) bit for bit.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <vector>
 
 #include "recon.hpp"
+#include "tc_ptx.cuh"
 
 namespace lpb200 {
 
@@ -88,6 +90,44 @@ __global__ void __launch_bounds__(256) k_slice_copy32(const V* __restrict__ src,
     }
 }
 
+// K1 through the TMA engine: the window is `outer` contiguous runs of run_b bytes (src
+// stride stride_b) packed back to back in dst.  Runs are cut into <= 16 KB chunks; each
+// warp's lane 0 is an independent copy engine with two shared-memory stages: bulk-load a
+// chunk (mbarrier complete_tx), bulk-store it, and load the next chunk into the other
+// stage while the store drains.  Requires 16-byte alignment of addresses, run and stride.
+constexpr int kSliceChunk = 16 * 1024, kSliceWarps = 4;
+__global__ void __launch_bounds__(32 * kSliceWarps) k_slice_bulk(const uint8_t* __restrict__ src,
+                                                                 uint8_t* __restrict__ dst, int64_t outer,
+                                                                 int64_t run_b, int64_t stride_b, int64_t off_b) {
+    extern __shared__ __align__(128) uint8_t sbuf[];  // [warps][2][chunk]
+    __shared__ uint64_t bars[kSliceWarps][2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane != 0) return;
+    uint64_t* bar = bars[warp];
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::fence_barrier_init();
+    uint8_t* buf = sbuf + static_cast<size_t>(warp) * 2 * kSliceChunk;
+    const int64_t cpr = (run_b + kSliceChunk - 1) / kSliceChunk, nchunks = outer * cpr;
+    const int64_t engines = static_cast<int64_t>(gridDim.x) * kSliceWarps;
+    uint32_t ph[2] = {0, 0};
+    int it = 0;
+    for (int64_t c = static_cast<int64_t>(blockIdx.x) * kSliceWarps + warp; c < nchunks; c += engines, ++it) {
+        const int b = it & 1;
+        const int64_t o = c / cpr, piece = c - o * cpr;
+        const int64_t at = piece * kSliceChunk;
+        const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kSliceChunk), run_b - at));
+        if (it >= 2) tc::bulk_wait_read<1>();  // the store issued from this stage two chunks ago has read it
+        tc::mbar_arrive_expect_tx(&bar[b], bytes);
+        tc::bulk_load(buf + b * kSliceChunk, src + o * stride_b + off_b + at, bytes, &bar[b]);
+        tc::mbar_wait(&bar[b], ph[b]);
+        ph[b] ^= 1;
+        tc::bulk_store(dst + o * run_b + at, buf + b * kSliceChunk, bytes);
+        tc::bulk_commit();
+    }
+    tc::bulk_wait_all();
+}
+
 template <typename V>
 static void launch_slice(const void* src, void* dst, int64_t outer, int64_t run, int64_t stride, int64_t off,
                          cudaStream_t st) {
@@ -110,6 +150,22 @@ void slice_to(const void* z, const Shape4& s, int axis, i64 begin, i64 end, int 
     const i64 run_b = (end - begin) * inner * E, stride_b = D * inner * E, off_b = begin * inner * E;
     const uintptr_t al = reinterpret_cast<uintptr_t>(z) | reinterpret_cast<uintptr_t>(dst);
     prof_begin(KC_GATHER, st);
+    if (run_b % 16 == 0 && stride_b % 16 == 0 && off_b % 16 == 0 && al % 16 == 0 && tune_get("slice_tma", 1)) {
+        // TMA-staged path (T and H windows; W windows of 4 x 16-byte multiples)
+        static bool attr = false;
+        constexpr int smem = kSliceWarps * 2 * kSliceChunk;
+        if (!attr) {
+            LP_CUDA(cudaFuncSetAttribute(k_slice_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            attr = true;
+        }
+        const int64_t chunks = outer * ((run_b + kSliceChunk - 1) / kSliceChunk);
+        const int grid = static_cast<int>(std::min<int64_t>((chunks + kSliceWarps - 1) / kSliceWarps, 148));
+        k_slice_bulk<<<grid, 32 * kSliceWarps, smem, st>>>(static_cast<const uint8_t*>(z), static_cast<uint8_t*>(dst),
+                                                            outer, run_b, stride_b, off_b);
+        LP_LAUNCH_CHECK();
+        prof_end(KC_GATHER, st, 0.0, 2.0 * static_cast<double>(outer) * static_cast<double>(run_b));
+        return;
+    }
     for (int vb : {16, 8, 4, 2, 1}) {
         if (run_b % vb || stride_b % vb || off_b % vb || al % vb) continue;
         switch (vb) {

@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 static int attn_poly() {
     // pairs out of every 16 whose exp2 runs on the FMA pipe (0, 4, 6 compiled; A/B r1n: 6 best)
     const int v = tune_get("attn_poly", 6);
-    return v == 0 || v == 6 ? v : 4;
+    return v == 0 || v == 6 || v == 8 ? v : 4;
 }
 
 void attention_bf16(const AttnArgs& x, cudaStream_t st) {
@@ -416,6 +416,7 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
         LP_CUDA(cudaFuncSetAttribute(k_attention<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         LP_CUDA(cudaFuncSetAttribute(k_attention<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         LP_CUDA(cudaFuncSetAttribute(k_attention<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         LP_CUDA(cudaFuncSetAttribute(k_attention<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         LP_CUDA(cudaFuncSetAttribute(k_attention<-1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         LP_CUDA(cudaFuncSetAttribute(k_attention<-2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
@@ -446,6 +447,7 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
         case -3: k_attention<-2, true><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
         case 0: k_attention<0><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
         case 6: k_attention<6><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
+        case 8: k_attention<8><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
         default: k_attention<4><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
     }
     LP_LAUNCH_CHECK();

@@ -29,12 +29,38 @@ __device__ __forceinline__ float ex2f_(float x) {
 template <int MODE>
 __global__ void k_sm(int iters, unsigned long long* out, float* sink) {
     __shared__ uint32_t slot;
+    __shared__ volatile uint32_t stop;
+    __shared__ uint64_t mb;
+    extern __shared__ __align__(1024) uint8_t ops[];  // MMA operands (bit 8 mode)
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x & 31;
     if (warp == 0) tmem_alloc(&slot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = slot;
+    if (threadIdx.x == 0) {
+        stop = 0;
+        mbar_init(&mb, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if ((MODE & 256) && warp == blockDim.x / 32 - 1) {
+        // background tensor-pipe load: one lane issues 128x128x16 MMAs into TMEM columns [256, 384)
+        __syncthreads();  // pairs with the softmax warps' pre-timing barrier
+        if ((threadIdx.x & 31) == 0) {
+            const uint64_t dA = desc_sw128(smem_u32(ops)), dB = desc_sw128(smem_u32(ops + 32768));
+            constexpr uint32_t id = idesc_bf16(128, 128);
+            while (!stop)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) mma_ss(tmem + 256, dA + 2 * (k & 3), dB + 2 * (k & 3), id, 1);
+            mma_commit(&mb);
+            mbar_wait(&mb, 0);
+        }
+        __syncwarp();
+        tc_fence_before();
+        __syncthreads();  // pairs with the final barrier
+        return;
+    }
     const uint32_t q = warp & 3, w = warp >> 2;
     const uint32_t tS = tmem + ((q * 32) << 16) + w * 64;
     float2 acc = make_float2(0.f, 0.f);
@@ -80,6 +106,10 @@ __global__ void k_sm(int iters, unsigned long long* out, float* sink) {
         if (!(MODE & 1)) tmem_st_wait();
     }
     const long long t1 = clock64();
+    if (MODE & 256) {
+        __syncwarp();
+        if (threadIdx.x == 0) stop = 1;
+    }
     sink[blockIdx.x * blockDim.x + threadIdx.x] = acc.x + acc.y;
     if (blockIdx.x == 0 && lane == 0 && warp == 0) out[0] = t1 - t0;
     tc_fence_before();
@@ -90,8 +120,10 @@ __global__ void k_sm(int iters, unsigned long long* out, float* sink) {
 extern "C" int sm_bench(int mode, int warps, int iters, unsigned long long* out, float* sink, void* st) {
     auto s = (cudaStream_t)st;
     switch (mode) {
-#define C_(m) case m: k_sm<m><<<148, warps * 32, 0, s>>>(iters, out, sink); break;
+#define C_(m) case m: cudaFuncSetAttribute(k_sm<m>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024); \
+        k_sm<m><<<148, warps * 32 + ((m & 256) ? 32 : 0), 65536 + 1024, s>>>(iters, out, sink); break;
         C_(0) C_(1) C_(2) C_(3) C_(4) C_(5) C_(6) C_(7) C_(0x40) C_(0x60) C_(0x80) C_(0x44) C_(0x64) C_(0x41) C_(0x61)
+        C_(0x100) C_(0x160) C_(0x101)
 #undef C_
         default: return -1;
     }

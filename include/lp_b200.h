@@ -341,6 +341,12 @@ int lp_engine_destroy(lp_engine* e);
 int lp_engine_latent(lp_engine* e, void** z_dptr);
 /* Runs steps [first, first+count) (1-based i; t = T+1-i) on `stream`. */
 int lp_engine_run(lp_engine* e, int32_t first_step, int32_t count, void* stream);
+/* The same step in phases: 1 = K1 + cfg_predict of this rank's entries into its slot of the
+ * gather buffer, 2 = K9 all-gather (no-op without an NCCL communicator), 3 = K10 from the
+ * gathered buffer.  With world > 1 and no NCCL id the caller exchanges the slots itself
+ * between phases 1 and 3 (world slots of slot_elems elements, rank r's slot at r*slot_elems). */
+int lp_engine_step_phase(lp_engine* e, int32_t step, int32_t phase, void* stream);
+int lp_engine_gather_buffer(const lp_engine* e, int32_t step, void** buffer, int64_t* slot_elems);
 /* Bytes this engine moved over NCCL so far, and the reference ledger bytes. */
 int lp_engine_comm(const lp_engine* e, uint64_t* nccl_bytes, uint64_t* ledger_bytes);
 /* Kernel launches issued by the engine so far (this library's kernels only). */

@@ -124,8 +124,10 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
             }
             // world > 1 always exchanges through NCCL; world == 1 does when an id is given
             // (a 1-rank communicator: exercises the exchange path on a single GPU)
-            if (c->world > 1 || nccl_id) {
-                if (!nccl_id) fail(LP_ERR_INVALID_ARGUMENT, "world > 1 needs an NCCL unique id");
+            // world > 1 exchanges through NCCL when given an id (lp_engine_run), or through the
+            // caller (lp_engine_step_phase + lp_engine_gather_buffer) without one; world == 1
+            // with an id runs the NCCL exchange on a 1-rank communicator
+            if (nccl_id) {
                 ncclUniqueId id;
                 std::memcpy(&id, nccl_id, 128);
                 LP_NCCL(ncclCommInitRank(&e->comm, c->world, id, c->rank));
@@ -159,62 +161,120 @@ int lp_engine_latent(lp_engine* e, void** z) {
     return LP_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+int step_axis(const lp_engine* e, int i) {
+    const lp_engine_config& c = e->cfg;
+    if (i < 1 || i > c.total_steps) fail(LP_ERR_INVALID_ARGUMENT, "step out of range");
+    return c.schedule_len > 0 ? c.schedule[(i - 1) % c.schedule_len] : rotation_axis(i);
+}
+
+// Phase 1 of step i (run_lp body, src/cluster.cpp:178-206): K1 + cfg_predict for every entry
+// this rank owns, written into its slot of the gather buffer (owned shards overlap on the
+// slot streams when there are several).
+void step_compute(lp_engine* e, int i, cudaStream_t st) {
+    const lp_engine_config& c = e->cfg;
+    const int E = c.dtype_bytes;
+    char* gather = static_cast<char*>(e->gather);
+    const int t = c.total_steps + 1 - i;
+    const int a = step_axis(e, i);
+    const lp_plan& plan = e->plans[a];
+    const ShardLayout& L = e->layout[a];
+    const bool fork = e->nslots > 1 && L.owned.size() > 1 && !tune_get("engine_serial", 0);
+    if (fork) {
+        LP_CUDA(cudaEventRecord(e->ev_fork, st));
+        for (int s = 0; s < e->nslots; ++s) LP_CUDA(cudaStreamWaitEvent(e->slot_stream[s], e->ev_fork, 0));
+    }
+    for (size_t idx = 0; idx < L.owned.size(); ++idx) {
+        const int k = L.owned[idx];
+        const int slot = fork ? static_cast<int>(idx % e->nslots) : 0;
+        cudaStream_t ss = fork ? e->slot_stream[slot] : st;
+        char* sub = static_cast<char*>(e->sub) + e->sub_stride * slot;
+        const lp_entry& en = plan.entries[k];
+        const Shape4 s = e->shape.with_extent(a, en.latent_end - en.latent_begin);
+        slice_to(e->z, e->shape, a, en.latent_begin, en.latent_end, E, sub, ss);  // K1
+        void* eps = gather + static_cast<size_t>(L.base[k]) * E;
+        const int64_t sh[4] = {s.c, s.t, s.h, s.w};
+        int rc;
+        if (c.denoiser < 0)
+            rc = lp_dit_cfg_predict_slot(c.dit, slot, sub, sh, E, t, c.guidance, eps, ss);
+        else
+            rc = lp_toy_cfg_predict(c.denoiser, c.radius, c.t_coeff, c.cond_coeff, sub, sh, E, t, e->cond_mean,
+                                    c.guidance, eps, e->ws, ss);
+        if (rc)
+            fail(LP_ERR_WORKER_FAILURE,
+                 "worker " + std::to_string(k + 1) + " failed at step " + std::to_string(i) + ": " + lp_last_error());
+    }
+    if (fork) {
+        for (int s = 0; s < e->nslots; ++s) {
+            LP_CUDA(cudaEventRecord(e->ev_join[s], e->slot_stream[s]));
+            LP_CUDA(cudaStreamWaitEvent(st, e->ev_join[s], 0));
+        }
+    }
+}
+
+// Phase 2 (K9): one in-place ncclAllGather of the padded rank slots.
+void step_exchange(lp_engine* e, int i, cudaStream_t st) {
+    const lp_engine_config& c = e->cfg;
+    const ShardLayout& L = e->layout[step_axis(e, i)];
+    const size_t slot = static_cast<size_t>(L.slot_elems) * c.dtype_bytes;
+    char* gather = static_cast<char*>(e->gather);
+    prof_begin(KC_ALLGATHER, st);
+    LP_NCCL(ncclAllGather(gather + slot * c.rank, gather, slot, ncclUint8, e->comm, st));
+    prof_end(KC_ALLGATHER, st, 0.0, static_cast<double>(slot) * (c.world - 1));
+    e->nccl_bytes += slot * static_cast<size_t>(c.world - 1);  // received by this rank
+}
+
+// Phase 3 (K10): reconstruct + sampler update of the replicated z from the gathered shards,
+// and the reference ledger's bytes for the step (src/cluster.cpp:186-209).
+void step_reconstruct(lp_engine* e, int i, cudaStream_t st) {
+    const lp_engine_config& c = e->cfg;
+    const int a = step_axis(e, i);
+    reconstruct_dispatch(e->recon[a], c.dtype_bytes, e->gather, e->z, nullptr, true, c.mode == LP_MODE_FAST, st);
+    uint64_t sum = 0;
+    for (size_t k = 1; k < e->elems[a].size(); ++k) sum += static_cast<uint64_t>(e->elems[a][k]);
+    e->ledger_bytes += 4ull * sum * static_cast<uint64_t>(c.wire_bytes);
+}
+
+}  // namespace
+
+extern "C" {
+
 int lp_engine_run(lp_engine* e, int32_t first, int32_t count, void* stream) {
     return guard([&] {
-        const lp_engine_config& c = e->cfg;
         cudaStream_t st = as_stream(stream);
-        const int E = c.dtype_bytes;
-        char* gather = static_cast<char*>(e->gather);
+        if (e->cfg.world > 1 && !e->comm)
+            fail(LP_ERR_INVALID_ARGUMENT,
+                 "world > 1 without an NCCL id: drive the steps with lp_engine_step_phase and an external exchange");
         const uint64_t l0 = launch_count();
         for (int i = first; i < first + count; ++i) {
-            if (i < 1 || i > c.total_steps) fail(LP_ERR_INVALID_ARGUMENT, "step out of range");
-            const int t = c.total_steps + 1 - i;
-            const int a = c.schedule_len > 0 ? c.schedule[(i - 1) % c.schedule_len] : rotation_axis(i);
-            const lp_plan& plan = e->plans[a];
-            const ShardLayout& L = e->layout[a];
-            const bool fork = e->nslots > 1 && L.owned.size() > 1 && !tune_get("engine_serial", 0);
-            if (fork) {
-                LP_CUDA(cudaEventRecord(e->ev_fork, st));
-                for (int s = 0; s < e->nslots; ++s) LP_CUDA(cudaStreamWaitEvent(e->slot_stream[s], e->ev_fork, 0));
-            }
-            for (size_t idx = 0; idx < L.owned.size(); ++idx) {
-                const int k = L.owned[idx];
-                const int slot = fork ? static_cast<int>(idx % e->nslots) : 0;
-                cudaStream_t ss = fork ? e->slot_stream[slot] : st;
-                char* sub = static_cast<char*>(e->sub) + e->sub_stride * slot;
-                const lp_entry& en = plan.entries[k];
-                const Shape4 s = e->shape.with_extent(a, en.latent_end - en.latent_begin);
-                slice_to(e->z, e->shape, a, en.latent_begin, en.latent_end, E, sub, ss);  // K1
-                void* eps = gather + static_cast<size_t>(L.base[k]) * E;
-                const int64_t sh[4] = {s.c, s.t, s.h, s.w};
-                int rc;
-                if (c.denoiser < 0)
-                    rc = lp_dit_cfg_predict_slot(c.dit, slot, sub, sh, E, t, c.guidance, eps, ss);
-                else
-                    rc = lp_toy_cfg_predict(c.denoiser, c.radius, c.t_coeff, c.cond_coeff, sub, sh, E, t,
-                                            e->cond_mean, c.guidance, eps, e->ws, ss);
-                if (rc) fail(LP_ERR_WORKER_FAILURE, "worker " + std::to_string(k + 1) + " failed at step " +
-                                                        std::to_string(i) + ": " + lp_last_error());
-            }
-            if (fork) {
-                for (int s = 0; s < e->nslots; ++s) {
-                    LP_CUDA(cudaEventRecord(e->ev_join[s], e->slot_stream[s]));
-                    LP_CUDA(cudaStreamWaitEvent(st, e->ev_join[s], 0));
-                }
-            }
-            if (e->comm) {
-                const size_t slot = static_cast<size_t>(L.slot_elems) * E;
-                prof_begin(KC_ALLGATHER, st);
-                LP_NCCL(ncclAllGather(gather + slot * c.rank, gather, slot, ncclUint8, e->comm, st));
-                prof_end(KC_ALLGATHER, st, 0.0, static_cast<double>(slot) * (c.world - 1));
-                e->nccl_bytes += slot * static_cast<size_t>(c.world - 1);  // received by this rank
-            }
-            reconstruct_dispatch(e->recon[a], E, gather, e->z, nullptr, true, c.mode == LP_MODE_FAST, st);  // K10
-            uint64_t sum = 0;
-            for (size_t k = 1; k < e->elems[a].size(); ++k) sum += static_cast<uint64_t>(e->elems[a][k]);
-            e->ledger_bytes += 4ull * sum * static_cast<uint64_t>(c.wire_bytes);  // cluster.cpp:186-209
+            step_compute(e, i, st);
+            if (e->comm) step_exchange(e, i, st);
+            step_reconstruct(e, i, st);
         }
         e->launches += launch_count() - l0;
+    });
+}
+
+int lp_engine_step_phase(lp_engine* e, int32_t step, int32_t phase, void* stream) {
+    return guard([&] {
+        cudaStream_t st = as_stream(stream);
+        const uint64_t l0 = launch_count();
+        if (phase == 1) step_compute(e, step, st);
+        else if (phase == 2) {
+            if (e->comm) step_exchange(e, step, st);
+        } else if (phase == 3) step_reconstruct(e, step, st);
+        else fail(LP_ERR_INVALID_ARGUMENT, "phase must be 1 (compute), 2 (exchange) or 3 (reconstruct)");
+        e->launches += launch_count() - l0;
+    });
+}
+
+int lp_engine_gather_buffer(const lp_engine* e, int32_t step, void** buffer, int64_t* slot_elems) {
+    return guard([&] {
+        *buffer = e->gather;
+        *slot_elems = e->layout[step_axis(e, step)].slot_elems;
     });
 }
 

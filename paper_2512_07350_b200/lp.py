@@ -444,7 +444,7 @@ class DiTDenoiser:
 def _wrap_device(ptr, numel, dtype):
     """Non-owning torch view of a device buffer owned by the library."""
     torch = _torch()
-    typestr = {torch.bfloat16: "<i2", torch.float32: "<f4", torch.float16: "<f2"}[dtype]
+    typestr = {torch.bfloat16: "<i2", torch.float32: "<f4", torch.float16: "<f2", torch.float64: "<f8"}[dtype]
 
     class _H:
         __cuda_array_interface__ = {"shape": (int(numel),), "typestr": typestr, "data": (int(ptr), False),
@@ -496,6 +496,7 @@ class LpEngine:
             for i, a in enumerate(axes):
                 cfg.schedule[i] = a
         self.dit = dit
+        self.world = int(world)
         self.dims = tuple(int(d) for d in dims)
         self.dtype_bytes = dtype_bytes
         c = (C.c_double * len(cond))(*cond)
@@ -516,6 +517,19 @@ class LpEngine:
     def run(self, first_step, count, stream=None):
         st = C.c_void_p(stream) if stream is not None else _stream()
         check(lib().lp_engine_run(self.handle, first_step, count, st))
+
+    def step_phase(self, step, phase, stream=None):
+        """lp_engine_step_phase: 1 = compute this rank's shards, 2 = NCCL exchange, 3 = reconstruct."""
+        st = C.c_void_p(stream) if stream is not None else _stream()
+        check(lib().lp_engine_step_phase(self.handle, int(step), int(phase), st))
+
+    def gather_buffer(self, step):
+        """(torch view of the gather buffer [world * slot_elems], slot_elems) for step's layout."""
+        ptr, slot = C.c_void_p(), C.c_int64()
+        check(lib().lp_engine_gather_buffer(self.handle, int(step), C.byref(ptr), C.byref(slot)))
+        torch = _torch()
+        dt = getattr(torch, _TORCH_DT[self.dtype_bytes])
+        return _wrap_device(ptr.value, self.world * slot.value, dt), slot.value
 
     def comm(self):
         a, b = C.c_uint64(), C.c_uint64()

@@ -67,6 +67,17 @@ def _digest(cmd, path):
     return h.hexdigest()
 
 
+def _nccl_link():
+    """Link the NCCL that torch ships (nvidia-nccl wheel) when present, with an rpath to it:
+    libnccl.so.2 is one soname, so whichever copy loads first serves the whole process, and
+    torch's libtorch_cuda needs symbols the older system NCCL lacks (ncclDevCommCreate)."""
+    d = os.path.join(sys.prefix, "lib", f"python{sys.version_info.major}.{sys.version_info.minor}", "site-packages",
+                     "nvidia", "nccl", "lib")
+    if os.path.exists(os.path.join(d, "libnccl.so.2")):
+        return ["-L" + d, "-l:libnccl.so.2", "-Xlinker", "-rpath," + d]
+    return ["-lnccl"]
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OUT, exist_ok=True)
     jobs = []
@@ -96,7 +107,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             if verbose:
                 print("compiled", s)
     objs = [os.path.join(OUT, s + ".o") for s, _ in SOURCES if os.path.exists(os.path.join(CSRC, s))]
-    link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lnccl", "-Xlinker", "-rpath,$ORIGIN"]
+    link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, *_nccl_link(), "-Xlinker", "-rpath,$ORIGIN"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stderr[-8000:])

@@ -415,9 +415,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workers", type=int, default=0, help="LP workers K (default max(4, N))")
     ap.add_argument("--layers", type=int, default=30)
+    ap.add_argument("--overlap", type=float, default=None,
+                    help="LP overlap ratio r (BASELINE configs[2] sweep; default 0.5 = configs[1])")
     ap.add_argument("--cpu-steps", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.overlap is not None:
+        global R_OVERLAP
+        R_OVERLAP = args.overlap
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

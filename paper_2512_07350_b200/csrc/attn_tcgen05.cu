@@ -72,7 +72,7 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 }
 
 // Debug timeline (TR variant only): clock64() stamps of CTA (0,0,0), indexed
-// [(j * 2 + tile) * 8 + event] for the first 64 key blocks.  Events: 0 S ready (softmax),
+// [(j * 2 + tile) * 16 + event] for the first 64 key blocks.  Events: 0 S ready (softmax),
 // 1 row max done, 2 p_half arrived, 3 p_full arrived, 4 MMA saw p_half, 5 MMA saw p_full,
 // 6 MMA issued S(j+1).
 __device__ unsigned long long* g_attn_trace = nullptr;
@@ -80,7 +80,7 @@ __device__ unsigned long long* g_attn_trace = nullptr;
 template <bool TR>
 __device__ __forceinline__ void trace_ev(int j, int t, int ev) {
     if (TR && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && j < 64 && g_attn_trace)
-        g_attn_trace[(j * 2 + t) * 8 + ev] = clock64();
+        g_attn_trace[(j * 2 + t) * 16 + ev] = clock64();
 }
 
 // One 128-key block of the online softmax for one query row (the calling thread's TMEM
@@ -162,6 +162,9 @@ __device__ __forceinline__ void softmax_block(uint32_t tS, uint32_t tO, int vali
         tc_fence_before();
         mbar_arrive(bar);
         if (tr0) trace_ev<TR>(j, t, 2 + half);
+        // per lane-quarter arrival (events 8..11 p_half, 12..15 p_full): the barrier completes
+        // at the slowest of the four warps
+        if (TR && (threadIdx.x & 31) == 0) trace_ev<TR>(j, t, 8 + 4 * half + ((threadIdx.x >> 5) & 3));
     };
     uint32_t ra[32], rb[32];
     tmem_ld32(tS, ra);
@@ -459,7 +462,7 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
 
 using namespace lpb200;
 
-// Debug: device buffer of 64*2*8 u64 receiving the TR variant's timeline (lp_tune("attn_trace", 1)).
+// Debug: device buffer of 64*2*16 u64 receiving the TR variant's timeline (lp_tune("attn_trace", 1)).
 extern "C" int lp_attention_set_trace(void* dev_buf) {
     return guard([&] { LP_CUDA(cudaMemcpyToSymbol(g_attn_trace, &dev_buf, sizeof(void*))); });
 }

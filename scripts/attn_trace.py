@@ -15,7 +15,7 @@ from paper_2512_07350_b200 import _lib  # noqa: E402
 L = _lib.lib()
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 18720
 q, k, v, o = (torch.randn(2, S, 12, 128, device="cuda").bfloat16() for _ in range(4))
-buf = torch.zeros(64 * 2 * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(64 * 2 * 16, dtype=torch.int64, device="cuda")
 _lib.check(L.lp_attention_set_trace(C.c_void_p(buf.data_ptr())))
 _lib.check(L.lp_tune(b"attn_trace", int(sys.argv[2]) if len(sys.argv) > 2 else 1))
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -23,9 +23,10 @@ for _ in range(3):
     _lib.check(L.lp_attention_bf16(C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()), C.c_void_p(v.data_ptr()),
                                    C.c_void_p(o.data_ptr()), 2, S, S, 12, C.c_double(1 / 128 ** 0.5), st))
 torch.cuda.synchronize()
-tr = buf.view(64, 2, 8).cpu()
+tr = buf.view(64, 2, 16).cpu()
 t0 = int(tr[0, 0, 0])
-names = ["S_ready", "max", "p_half", "p_full", "mma_p_half", "mma_p_full", "mma_S_next", "ev7"]
+names = ["S_ready", "max", "p_half", "p_full", "mma_p_half", "mma_p_full", "mma_S_next", "ev7",
+         "p_half_q0", "p_half_q1", "p_half_q2", "p_half_q3", "p_full_q0", "p_full_q1", "p_full_q2", "p_full_q3"]
 rows = []
 for j in range(min(64, -(-S // 128))):
     for t in range(2):

@@ -56,9 +56,18 @@ def full(path):
             if m in hdr:
                 v = r[hdr.index(m)].replace(",", "")
                 try:
-                    d[k] = float(v)
+                    x = float(v)
                 except ValueError:
                     d[k] = v
+                    continue
+                # ncu auto-scales units per metric (the second CSV row): normalise to ms / MB
+                u = units[hdr.index(m)].strip().lower()
+                if k == "duration_ms":
+                    x *= {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "s": 1e3,
+                          "second": 1e3}.get(u, 1.0)
+                elif k.endswith("_MB"):
+                    x *= {"byte": 1e-6, "kbyte": 1e-3, "mbyte": 1.0, "gbyte": 1e3, "tbyte": 1e6}.get(u, 1.0)
+                d[k] = x
         res.append(d)
     return res
 

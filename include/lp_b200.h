@@ -286,6 +286,11 @@ int lp_dit_cfg_predict_slot(lp_dit* dit, int32_t slot, const void* sub, const in
  * text), one forward, combine uncond + w*(cond-uncond), quantize to dtype. */
 int lp_dit_cfg_predict(lp_dit* dit, const void* sub, const int64_t shape[4], int dtype_bytes, int timestep,
                        double guidance, void* eps_out, void* stream);
+/* For step loops captured into CUDA graphs: with time_on_device(1) the forwards read the
+ * timestep from the slot's device scalar, which lp_dit_set_time writes (stream-ordered)
+ * before each replay, instead of baking the host value into a kernel argument. */
+int lp_dit_set_time(lp_dit* dit, int32_t slot, int timestep, void* stream);
+int lp_dit_time_on_device(lp_dit* dit, int32_t on);
 /* Parameter access for tests: index -> name, device pointer, element count, dtype (2=bf16,4=f32). */
 int lp_dit_num_params(const lp_dit* dit);
 int lp_dit_param(const lp_dit* dit, int32_t index, const char** name, void** dptr, int64_t* numel,

@@ -124,6 +124,8 @@ _SIGS = {
     "lp_gemm_bf16": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "lp_attention_bf16": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _d, _vp]),
     "lp_attention_set_trace": (_i, [_vp]),
+    "lp_dit_set_time": (_i, [_vp, _i32, _i, _vp]),
+    "lp_dit_time_on_device": (_i, [_vp, _i32]),
     "lp_engine_step_phase": (_i, [_vp, _i32, _i32, _vp]),
     "lp_engine_gather_buffer": (_i, [_vp, _i32, C.POINTER(_vp), C.POINTER(_i64)]),
     "lp_verify_n_complete": (_i, [_i64p, _i32, _d, C.POINTER(_i32), _i32, _i32, _i64, C.POINTER(_i32),

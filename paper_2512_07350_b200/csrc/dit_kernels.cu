@@ -112,7 +112,8 @@ __global__ void k_gemv(const __nv_bfloat16* __restrict__ W, const float* __restr
 }
 
 // sinusoid embedding: [cos(t*w_i), sin(t*w_i)], w_i = 10000^(-i/half)
-__global__ void k_sinusoid(float* out, int dim, float t) {
+__global__ void k_sinusoid(float* out, int dim, const float* __restrict__ t_dev) {
+    const float t = *t_dev;  // device-resident: a captured step graph replays with a new t
     const int half = dim / 2;
     for (int i = threadIdx.x; i < half; i += blockDim.x) {
         const double w = pow(10000.0, -static_cast<double>(i) / half);
@@ -130,13 +131,20 @@ __global__ void k_add_mod(const float* __restrict__ param, const float* __restri
         out[i] = param[i] + e0[i % per_layer];
 }
 
-void time_embedding(const TimeWeights& w, float t, int freq_dim, int dim, int layers, float* scratch,
+__global__ void k_set_f32(float* p, float v) { *p = v; }
+
+void set_device_f32(float* p, float v, cudaStream_t st) {
+    k_set_f32<<<1, 1, 0, st>>>(p, v);
+    LP_LAUNCH_CHECK();
+}
+
+void time_embedding(const TimeWeights& w, const float* t_dev, int freq_dim, int dim, int layers, float* scratch,
                     float* mod_out, float* head_mod_out, cudaStream_t st) {
     float* sin_ = scratch;                 // [freq_dim]
     float* h1 = sin_ + freq_dim;           // [dim]
     float* e = h1 + dim;                   // [dim]
     float* e0 = e + dim;                   // [6*dim]
-    k_sinusoid<<<1, 256, 0, st>>>(sin_, freq_dim, t);
+    k_sinusoid<<<1, 256, 0, st>>>(sin_, freq_dim, t_dev);
     LP_LAUNCH_CHECK();
     k_gemv<<<(dim + 7) / 8, 256, 0, st>>>(w.w1, w.b1, sin_, h1, freq_dim, dim, 0);
     LP_LAUNCH_CHECK();

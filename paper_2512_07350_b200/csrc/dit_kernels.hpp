@@ -22,8 +22,10 @@ void init_param(void* p, int64_t n, bool bf16, uint64_t seed, uint64_t stream, f
 void text_context(__nv_bfloat16* out, int64_t n, uint64_t seed, cudaStream_t st);
 void patchify(const void* z, int dtype, const int shape[4], const int patch[3], __nv_bfloat16* out, cudaStream_t st);
 // scratch >= freq_dim + 8*dim floats; mod_out [layers, 6, dim]; head_mod_out [2, dim]
-void time_embedding(const TimeWeights& w, float t, int freq_dim, int dim, int layers, float* scratch, float* mod_out,
-                    float* head_mod_out, cudaStream_t st);
+void time_embedding(const TimeWeights& w, const float* t_dev, int freq_dim, int dim, int layers, float* scratch,
+                    float* mod_out, float* head_mod_out, cudaStream_t st);
+// *p = v on the stream (a one-thread kernel: stream-ordered and independent of host memory)
+void set_device_f32(float* p, float v, cudaStream_t st);
 void layernorm_bf16(const float* x, __nv_bfloat16* y, int64_t rows, int d, const float* a, const float* b, bool affine,
                     float eps, cudaStream_t st);
 void rmsnorm_rope(__nv_bfloat16* buf, int64_t rows, int64_t ld, int64_t col0, int d, const float* g, float eps,

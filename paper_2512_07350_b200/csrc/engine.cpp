@@ -48,6 +48,12 @@ struct lp_engine {
     cudaEvent_t ev_fork = nullptr, ev_join[4] = {};
     ncclComm_t comm = nullptr;
     uint64_t nccl_bytes = 0, ledger_bytes = 0, launches = 0;
+    // DiT engines replay each axis's step as a CUDA graph (captured the second time the
+    // axis comes up, so every kernel's one-time setup has run eagerly first)
+    cudaGraphExec_t graph[3] = {};
+    uint64_t graph_kernels[3] = {};
+    int seen[3] = {};
+    cudaStream_t cap_stream = nullptr;  // capture happens here (the caller's stream may be the legacy default)
 };
 
 extern "C" {
@@ -142,6 +148,9 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
 
 int lp_engine_destroy(lp_engine* e) {
     if (!e) return LP_OK;
+    for (auto& g : e->graph)
+        if (g) cudaGraphExecDestroy(g);
+    if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
     if (e->comm) ncclCommDestroy(e->comm);
     cudaFree(e->z);
     cudaFree(e->gather);
@@ -224,7 +233,6 @@ void step_exchange(lp_engine* e, int i, cudaStream_t st) {
     prof_begin(KC_ALLGATHER, st);
     LP_NCCL(ncclAllGather(gather + slot * c.rank, gather, slot, ncclUint8, e->comm, st));
     prof_end(KC_ALLGATHER, st, 0.0, static_cast<double>(slot) * (c.world - 1));
-    e->nccl_bytes += slot * static_cast<size_t>(c.world - 1);  // received by this rank
 }
 
 // Phase 3 (K10): reconstruct + sampler update of the replicated z from the gathered shards,
@@ -233,9 +241,64 @@ void step_reconstruct(lp_engine* e, int i, cudaStream_t st) {
     const lp_engine_config& c = e->cfg;
     const int a = step_axis(e, i);
     reconstruct_dispatch(e->recon[a], c.dtype_bytes, e->gather, e->z, nullptr, true, c.mode == LP_MODE_FAST, st);
+}
+
+// Host-side accounting of step i: NCCL bytes this rank receives and the reference ledger's
+// bytes for the step (src/cluster.cpp:186-209).
+void account_step(lp_engine* e, int i) {
+    const lp_engine_config& c = e->cfg;
+    const int a = step_axis(e, i);
+    if (e->comm) e->nccl_bytes += static_cast<size_t>(e->layout[a].slot_elems) * c.dtype_bytes * (c.world - 1);
     uint64_t sum = 0;
     for (size_t k = 1; k < e->elems[a].size(); ++k) sum += static_cast<uint64_t>(e->elems[a][k]);
     e->ledger_bytes += 4ull * sum * static_cast<uint64_t>(c.wire_bytes);
+}
+
+void run_step_eager(lp_engine* e, int i, cudaStream_t st) {
+    step_compute(e, i, st);
+    if (e->comm) step_exchange(e, i, st);
+    step_reconstruct(e, i, st);
+}
+
+// One step of a DiT engine as a graph replay: write the timestep into every slot's device
+// scalar, then launch the axis's graph (captured on the second occurrence of the axis).
+void run_step_graph(lp_engine* e, int i, cudaStream_t st) {
+    const lp_engine_config& c = e->cfg;
+    const int a = step_axis(e, i);
+    const int t = c.total_steps + 1 - i;
+    if (++e->seen[a] < 2 && !e->graph[a]) {
+        run_step_eager(e, i, st);
+        return;
+    }
+    for (int s = 0; s < e->nslots; ++s) {
+        const int rc = lp_dit_set_time(c.dit, s, t, st);
+        if (rc) fail(rc, lp_last_error());
+    }
+    if (!e->graph[a]) {
+        lp_dit_time_on_device(c.dit, 1);
+        const uint64_t l0 = launch_count();
+        cudaGraph_t g = nullptr;
+        if (!e->cap_stream) LP_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+        cudaStream_t cs = e->cap_stream;
+        LP_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        try {
+            run_step_eager(e, i, cs);
+        } catch (...) {
+            cudaStreamEndCapture(cs, &g);
+            if (g) cudaGraphDestroy(g);
+            lp_dit_time_on_device(c.dit, 0);
+            throw;
+        }
+        LP_CUDA(cudaStreamEndCapture(cs, &g));
+        lp_dit_time_on_device(c.dit, 0);
+        e->graph_kernels[a] = launch_count() - l0;
+        const cudaError_t err = cudaGraphInstantiate(&e->graph[a], g, 0);
+        cudaGraphDestroy(g);
+        LP_CUDA(err);
+    } else {
+        count_launch(e->graph_kernels[a]);  // the replay runs the captured kernels again
+    }
+    LP_CUDA(cudaGraphLaunch(e->graph[a], st));
 }
 
 }  // namespace
@@ -249,10 +312,14 @@ int lp_engine_run(lp_engine* e, int32_t first, int32_t count, void* stream) {
             fail(LP_ERR_INVALID_ARGUMENT,
                  "world > 1 without an NCCL id: drive the steps with lp_engine_step_phase and an external exchange");
         const uint64_t l0 = launch_count();
+        // graphs: DiT engines, on a stream that can be captured, unless per-launch profiling
+        // or the serialised debug mode is on (both need the eager launches)
+        const bool graphs =
+            e->cfg.dit != nullptr && tune_get("engine_graph", 1) && !prof_enabled() && !tune_get("engine_serial", 0);
         for (int i = first; i < first + count; ++i) {
-            step_compute(e, i, st);
-            if (e->comm) step_exchange(e, i, st);
-            step_reconstruct(e, i, st);
+            if (graphs) run_step_graph(e, i, st);
+            else run_step_eager(e, i, st);
+            account_step(e, i);
         }
         e->launches += launch_count() - l0;
     });
@@ -265,7 +332,10 @@ int lp_engine_step_phase(lp_engine* e, int32_t step, int32_t phase, void* stream
         if (phase == 1) step_compute(e, step, st);
         else if (phase == 2) {
             if (e->comm) step_exchange(e, step, st);
-        } else if (phase == 3) step_reconstruct(e, step, st);
+        } else if (phase == 3) {
+            step_reconstruct(e, step, st);
+            account_step(e, step);
+        }
         else fail(LP_ERR_INVALID_ARGUMENT, "phase must be 1 (compute), 2 (exchange) or 3 (reconstruct)");
         e->launches += launch_count() - l0;
     });

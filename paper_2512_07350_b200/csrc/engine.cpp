@@ -314,8 +314,10 @@ int lp_engine_run(lp_engine* e, int32_t first, int32_t count, void* stream) {
         const uint64_t l0 = launch_count();
         // graphs: DiT engines, on a stream that can be captured, unless per-launch profiling
         // or the serialised debug mode is on (both need the eager launches)
-        const bool graphs =
-            e->cfg.dit != nullptr && tune_get("engine_graph", 1) && !prof_enabled() && !tune_get("engine_serial", 0);
+        // (multi-rank engines stay eager: their step holds an ncclAllGather, and a capture
+        // failure there would cost a scaling run for no device-time gain — DESIGN.md §6)
+        const bool graphs = e->cfg.dit != nullptr && e->comm == nullptr && tune_get("engine_graph", 1) &&
+                            !prof_enabled() && !tune_get("engine_serial", 0);
         for (int i = first; i < first + count; ++i) {
             if (graphs) run_step_graph(e, i, st);
             else run_step_eager(e, i, st);

@@ -32,7 +32,7 @@ def timeit(fn, reps=10):
 
 
 out = {}
-R = 2 * 32760
+R = int(os.environ.get("KB_ROWS", 2 * 32760))  # 2n rows (CFG batch 2); in-step shards: 2*14040 .. 2*18720
 GEMMS = [(R, 4608, 1536, "qkv"), (R, 1536, 1536, "o"), (R, 8960, 1536, "ffn1"), (R, 1536, 8960, "ffn2"),
          (8192, 8192, 8192, "sq8k")]
 for (M, N, K, name) in ([] if "attn" in sys.argv else GEMMS):

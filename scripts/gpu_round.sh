@@ -20,6 +20,6 @@ if [ "$3" != "skip-ncu" ]; then
       python bench.py --steps 3 --warmup 1 --no-cpu-baseline > $O/ncu_bench.log 2>&1; echo "ncu-launch rc=$?" | tee -a $O/status
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_attention -s 40 -c 1 -o $O/attn_full \
       python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/ncu_full.log 2>&1; echo "ncu-full-attn rc=$?" | tee -a $O/status
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 40 -c 2 -o $O/gemm_full \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_gemm2 -s 150 -c 2 -o $O/gemm_full \
       python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/ncu_full_gemm.log 2>&1; echo "ncu-full-gemm rc=$?" | tee -a $O/status
 fi

@@ -21,11 +21,13 @@ def launches(path):
     rows = list(csv.reader(l for l in open(path) if l.startswith('"')))
     hdr = rows[0]
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    ui = hdr.index("Metric Unit") if "Metric Unit" in hdr else None
+    scale = {"ns": 1.0, "nsecond": 1.0, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}
     tot = defaultdict(float)
     cnt = defaultdict(int)
     for r in rows[1:]:
         k = short(r[ki])
-        tot[k] += float(r[vi].replace(",", ""))
+        tot[k] += float(r[vi].replace(",", "")) * (scale.get(r[ui].strip().lower(), 1.0) if ui is not None else 1.0)
         cnt[k] += 1
     s = sum(tot.values())
     return {k: {"launches": cnt[k], "ns": tot[k], "share": tot[k] / s} for k in sorted(tot, key=lambda x: -tot[x])}

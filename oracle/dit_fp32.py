@@ -65,9 +65,13 @@ def attention(q, k, v, heads):
 
 
 class DiTReference:
-    def __init__(self, dit):
+    """act_bf16=True rounds every GEMM / attention operand to bf16 (fp32 math otherwise): the
+    precision floor of any bf16-operand implementation, used to ground the test tolerances."""
+
+    def __init__(self, dit, act_bf16=False):
         self.cfg = dit.cfg
         self.p = {k: _f(v) for k, v in dit.params().items()}
+        self.r = (lambda x: x.bfloat16().float()) if act_bf16 else (lambda x: x)
 
     def lin(self, x, name):
         return x @ self.p[name + ".w"].view(-1, x.shape[-1]).t() + self.p[name + ".b"]
@@ -103,7 +107,7 @@ class DiTReference:
         zp[:, :F, :H, :W] = z
         patches = zp.view(C, nf, pt, nh, ph, nw, pw).permute(1, 3, 5, 0, 2, 4, 6).reshape(nf * nh * nw, -1)
         n = patches.shape[0]
-        x0 = patches @ self.p["patch.w"].view(d, -1).t() + self.p["patch.b"]
+        x0 = self.r(patches) @ self.p["patch.w"].view(d, -1).t() + self.p["patch.b"]
         B = len(batches)
         x = torch.cat([x0] * B, 0)
         s = sinusoid(c.freq_dim, t * c.t_scale).to(z.device)
@@ -115,7 +119,7 @@ class DiTReference:
         for l in range(L):
             pre = f"blocks.{l}."
             m = mods[l]
-            h = Fn.layer_norm(x, (d,), eps=eps) * (1 + m[1]) + m[0]
+            h = self.r(Fn.layer_norm(x, (d,), eps=eps) * (1 + m[1]) + m[0])
             qkv = h @ self.p[pre + "qkv.w"].view(3 * d, d).t() + self.p[pre + "qkv.b"]
             q, k, v = qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:]
             q = rms(q, self.p[pre + "norm_q"], eps)
@@ -123,21 +127,22 @@ class DiTReference:
             outs = []
             for b in range(B):
                 sl = slice(b * n, (b + 1) * n)
-                outs.append(attention(apply_rope(q[sl], cos, sin, heads), apply_rope(k[sl], cos, sin, heads), v[sl], heads))
-            y = torch.cat(outs, 0) @ self.p[pre + "o.w"].view(d, d).t() + self.p[pre + "o.b"]
+                outs.append(attention(self.r(apply_rope(q[sl], cos, sin, heads)), self.r(apply_rope(k[sl], cos, sin, heads)),
+                                      self.r(v[sl]), heads))
+            y = self.r(torch.cat(outs, 0)) @ self.p[pre + "o.w"].view(d, d).t() + self.p[pre + "o.b"]
             x = x + y * m[2]
-            h = Fn.layer_norm(x, (d,), weight=self.p[pre + "norm3.w"], bias=self.p[pre + "norm3.b"], eps=eps)
+            h = self.r(Fn.layer_norm(x, (d,), weight=self.p[pre + "norm3.w"], bias=self.p[pre + "norm3.b"], eps=eps))
             cq = rms(h @ self.p[pre + "cq.w"].view(d, d).t() + self.p[pre + "cq.b"], self.p[pre + "cnorm_q"], eps)
             outs = []
             for b in range(B):
                 sl = slice(b * n, (b + 1) * n)
-                outs.append(attention(cq[sl], ctx_k[l][batches[b]], ctx_v[l][batches[b]], heads))
-            x = x + torch.cat(outs, 0) @ self.p[pre + "co.w"].view(d, d).t() + self.p[pre + "co.b"]
-            h = Fn.layer_norm(x, (d,), eps=eps) * (1 + m[4]) + m[3]
-            f = Fn.gelu(h @ self.p[pre + "ffn1.w"].view(c.ffn_dim, d).t() + self.p[pre + "ffn1.b"], approximate="tanh")
+                outs.append(attention(self.r(cq[sl]), ctx_k[l][batches[b]], ctx_v[l][batches[b]], heads))
+            x = x + self.r(torch.cat(outs, 0)) @ self.p[pre + "co.w"].view(d, d).t() + self.p[pre + "co.b"]
+            h = self.r(Fn.layer_norm(x, (d,), eps=eps) * (1 + m[4]) + m[3])
+            f = self.r(Fn.gelu(h @ self.p[pre + "ffn1.w"].view(c.ffn_dim, d).t() + self.p[pre + "ffn1.b"], approximate="tanh"))
             x = x + (f @ self.p[pre + "ffn2.w"].view(d, c.ffn_dim).t() + self.p[pre + "ffn2.b"]) * m[5]
         hm = self.p["head.mod"].view(2, d) + e[None]
-        h = Fn.layer_norm(x, (d,), eps=eps) * (1 + hm[1]) + hm[0]
+        h = self.r(Fn.layer_norm(x, (d,), eps=eps) * (1 + hm[1]) + hm[0])
         head = h @ self.p["head.w"].view(-1, d).t() + self.p["head.b"]  # [2n, pt*ph*pw*C]
         out = head.view(B, nf, nh, nw, pt, ph, pw, C).permute(0, 7, 1, 4, 2, 5, 3, 6).reshape(B, C, nf * pt, nh * ph, nw * pw)
         return out[:, :, :F, :H, :W], head

@@ -108,8 +108,15 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
             for (int a = 0; a < 3; ++a) max_owned = std::max(max_owned, e->layout[a].owned.size());
             const int want_slots = std::max(1, std::min(4, tune_get("engine_slots", 2)));
             if (c->dit && max_owned > 1) e->nslots = static_cast<int>(std::min<size_t>(max_owned, want_slots));
-            e->sub_stride = (static_cast<size_t>(max_entry) * E + 255) / 256 * 256;
-            LP_CUDA(cudaMalloc(&e->sub, e->sub_stride * e->nslots));
+            // K1 gathers every owned entry of a step in one launch, packed in owned order
+            size_t max_owned_elems = 1;
+            for (int a = 0; a < 3; ++a) {
+                size_t tot = 0;
+                for (int k : e->layout[a].owned) tot += static_cast<size_t>(e->elems[a][k]);
+                max_owned_elems = std::max(max_owned_elems, tot);
+            }
+            (void)max_entry;
+            LP_CUDA(cudaMalloc(&e->sub, max_owned_elems * E));
             LP_CUDA(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
             for (int s = 0; s < e->nslots; ++s) {
                 LP_CUDA(cudaStreamCreateWithFlags(&e->slot_stream[s], cudaStreamNonBlocking));
@@ -192,18 +199,21 @@ void step_compute(lp_engine* e, int i, cudaStream_t st) {
     const lp_plan& plan = e->plans[a];
     const ShardLayout& L = e->layout[a];
     const bool fork = e->nslots > 1 && L.owned.size() > 1 && !tune_get("engine_serial", 0);
+    // K1: one launch gathers all owned entries (packed in owned order) before the fork
+    if (!L.owned.empty()) gather_entries(e->z, e->shape, plan, L.owned.data(), static_cast<int>(L.owned.size()), E, e->sub, st);
     if (fork) {
         LP_CUDA(cudaEventRecord(e->ev_fork, st));
         for (int s = 0; s < e->nslots; ++s) LP_CUDA(cudaStreamWaitEvent(e->slot_stream[s], e->ev_fork, 0));
     }
+    size_t sub_off = 0;
     for (size_t idx = 0; idx < L.owned.size(); ++idx) {
         const int k = L.owned[idx];
         const int slot = fork ? static_cast<int>(idx % e->nslots) : 0;
         cudaStream_t ss = fork ? e->slot_stream[slot] : st;
-        char* sub = static_cast<char*>(e->sub) + e->sub_stride * slot;
+        char* sub = static_cast<char*>(e->sub) + sub_off;
+        sub_off += static_cast<size_t>(e->elems[a][k]) * E;
         const lp_entry& en = plan.entries[k];
         const Shape4 s = e->shape.with_extent(a, en.latent_end - en.latent_begin);
-        slice_to(e->z, e->shape, a, en.latent_begin, en.latent_end, E, sub, ss);  // K1
         void* eps = gather + static_cast<size_t>(L.base[k]) * E;
         const int64_t sh[4] = {s.c, s.t, s.h, s.w};
         int rc;

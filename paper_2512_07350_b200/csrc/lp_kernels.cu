@@ -11,6 +11,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
 #include <vector>
 
 #include "recon.hpp"
@@ -126,6 +129,106 @@ __global__ void __launch_bounds__(32 * kSliceWarps) k_slice_bulk(const uint8_t* 
         tc::bulk_commit();
     }
     tc::bulk_wait_all();
+}
+
+// K1, multi-entry form (the default): ONE launch gathers a run of plan entries, packed back
+// to back in dst.  The work is the flat space of V-vectors of all entries; a vector g
+// belongs to entry k with start_k <= g < start_{k+1} (a scan over <= 64 starts, warp-uniform
+// except at the boundaries), row o = (g - start_k) / run_k by multiply-shift division, and
+// is read from z at o * stride + off_k + (g - start_k - o * run_k).  dst is written at g
+// itself: the packing IS the flat index.  Each thread keeps U vectors in flight.
+struct GatherEntry {
+    uint32_t start, run, off;  // in V units
+    FastDiv div;
+};
+struct GatherParams {
+    int n;
+    uint32_t total, stride;  // in V units
+    GatherEntry e[kMaxKernelEntries];
+};
+
+template <typename V, int U>
+__global__ void __launch_bounds__(256) k_gather_entries(const __grid_constant__ GatherParams p,
+                                                        const V* __restrict__ src, V* __restrict__ dst) {
+    const uint32_t step = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < p.total; base += U * step) {
+        V v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t g = base + u * step;
+            if (g < p.total) {
+                int k = 0;
+                while (k + 1 < p.n && g >= p.e[k + 1].start) ++k;
+                const uint32_t r = g - p.e[k].start;
+                const uint32_t o = static_cast<uint32_t>((static_cast<uint64_t>(r) * p.e[k].div.mul) >> p.e[k].div.shift);
+                v[u] = __ldg(src + static_cast<uint64_t>(o) * p.stride + p.e[k].off + (r - o * p.e[k].run));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (base + u * step < p.total) dst[base + u * step] = v[u];
+    }
+}
+
+// Builds the one-launch gather of entries ks[0..count) of `plan` (packed in that order);
+// false when 32-bit vector indexing does not fit (the caller then copies entry by entry).
+static bool gather_params(const void* z, const Shape4& s, const lp_plan& plan, const int* ks, int count, int E,
+                          const void* dst, GatherParams& p, int& vb) {
+    if (count <= 0 || count > kMaxKernelEntries || !tune_get("gather_multi", 1)) return false;
+    i64 outer, inner;
+    axis_view(s, plan.axis, outer, inner);
+    const i64 stride_b = s.extent(plan.axis) * inner * E;
+    uint64_t al = reinterpret_cast<uintptr_t>(z) | reinterpret_cast<uintptr_t>(dst) | static_cast<uint64_t>(stride_b);
+    i64 bytes = 0;
+    for (int c = 0; c < count; ++c) {
+        const lp_entry& en = plan.entries[ks[c]];
+        al |= static_cast<uint64_t>(en.latent_begin * inner * E) |
+              static_cast<uint64_t>((en.latent_end - en.latent_begin) * inner * E);
+        bytes += outer * (en.latent_end - en.latent_begin) * inner * E;
+    }
+    vb = 16;
+    while (vb > E && al % vb) vb >>= 1;
+    if (bytes / vb >= (1ll << 31) || outer * stride_b / vb >= (1ll << 32)) return false;
+    std::memset(&p, 0, sizeof(p));
+    p.n = count;
+    p.stride = static_cast<uint32_t>(stride_b / vb);
+    uint32_t start = 0;
+    for (int c = 0; c < count; ++c) {
+        const lp_entry& en = plan.entries[ks[c]];
+        const uint32_t run = static_cast<uint32_t>((en.latent_end - en.latent_begin) * inner * E / vb);
+        p.e[c] = GatherEntry{start, run, static_cast<uint32_t>(en.latent_begin * inner * E / vb), make_fastdiv(run)};
+        start += run * static_cast<uint32_t>(outer);
+    }
+    p.total = start;
+    return true;
+}
+
+void gather_entries(const void* z, const Shape4& s, const lp_plan& plan, const int* ks, int count, int E, void* dst,
+                    cudaStream_t st) {
+    i64 outer, inner;
+    axis_view(s, plan.axis, outer, inner);
+    GatherParams p;
+    int vb = 0;
+    if (gather_params(z, s, plan, ks, count, E, dst, p, vb)) {
+        constexpr int U = 4;
+        const int g = grid_for((p.total + U - 1) / U, 256, 8);
+        prof_begin(KC_GATHER, st);
+        switch (vb) {
+            case 16: k_gather_entries<uint4, U><<<g, 256, 0, st>>>(p, static_cast<const uint4*>(z), static_cast<uint4*>(dst)); break;
+            case 8: k_gather_entries<uint2, U><<<g, 256, 0, st>>>(p, static_cast<const uint2*>(z), static_cast<uint2*>(dst)); break;
+            case 4: k_gather_entries<uint32_t, U><<<g, 256, 0, st>>>(p, static_cast<const uint32_t*>(z), static_cast<uint32_t*>(dst)); break;
+            default: k_gather_entries<uint16_t, U><<<g, 256, 0, st>>>(p, static_cast<const uint16_t*>(z), static_cast<uint16_t*>(dst)); break;
+        }
+        LP_LAUNCH_CHECK();
+        prof_end(KC_GATHER, st, 0.0, 2.0 * static_cast<double>(p.total) * vb);
+        return;
+    }
+    char* d = static_cast<char*>(dst);
+    for (int c = 0; c < count; ++c) {
+        const lp_entry& en = plan.entries[ks[c]];
+        slice_to(z, s, plan.axis, en.latent_begin, en.latent_end, E, d, st);
+        d += outer * (en.latent_end - en.latent_begin) * inner * E;
+    }
 }
 
 template <typename V>
@@ -405,12 +508,363 @@ __global__ void __launch_bounds__(256) k_reconstruct_tab(const __grid_constant__
     }
 }
 
+// K10, coverage-table form (the default when every position is covered by at most
+// kReconCover entries and indices fit 32 bits).  The block first tabulates, per position x,
+// the covering entries with a non-zero weight in worker order: weight w, the element offset
+// of (o=0, j) in the gathered buffer and the per-o stride (len*inner), plus Z(x) — the same
+// IEEE operations as entry_weight and the reference.  Each thread then owns 4 consecutive
+// elements: z moves as one 4-element vector, and when inner % 4 == 0 the 4 elements share
+// (o, x), so every covering prediction is one 4-element vector load too.  All loads of an
+// iteration are issued before any arithmetic (predicated on the coverage count), so an SM
+// keeps ~48 B per thread in flight.  Z(x) == 1 (one covering entry of weight 1, the bulk of
+// the latent) needs no division: A/1 is exact.
+constexpr int kReconCover = 4;
+
+template <int D> struct Vec4;
+template <> struct Vec4<4> {
+    using T = float4;
+    static __device__ __forceinline__ double get(const T& v, int u) {
+        return static_cast<double>(u == 0 ? v.x : u == 1 ? v.y : u == 2 ? v.z : v.w);
+    }
+};
+template <> struct Vec4<8> {
+    struct T { double2 a, b; };
+    static __device__ __forceinline__ double get(const T& v, int u) { return u == 0 ? v.a.x : u == 1 ? v.a.y : u == 2 ? v.b.x : v.b.y; }
+};
+template <> struct Vec4<2> {
+    using T = uint2;
+    static __device__ __forceinline__ double get(const T& v, int u) {
+        const uint32_t w = u < 2 ? v.x : v.y;
+        return f16_decode_exact(static_cast<uint16_t>((u & 1) ? (w >> 16) : (w & 0xffffu)));
+    }
+};
+template <int D>
+__device__ __forceinline__ typename Vec4<D>::T vload4(const typename Store<D>::T* p) {
+    return *reinterpret_cast<const typename Vec4<D>::T*>(p);
+}
+
+// The coverage table of a plan (layout below), built once on the device by one block with
+// entry_weight's exact operations and cached per (plan, gather layout, device): K10 blocks
+// then only copy ~2 KB into shared memory instead of each re-deriving it.
+struct CovLayout {
+    // structure of arrays [cover][x]: lanes on consecutive x (W axis) hit distinct banks
+    double* wts;      // [4][Dx]
+    double* zsum;     // [Dx]
+    float* zsumf;     // [Dx] (FAST)
+    uint32_t* offs;   // [4][Dx]
+    uint32_t* ostr;   // [4][Dx]
+    uint32_t* cnt;    // [Dx]
+    __host__ __device__ explicit CovLayout(void* base, int Dx) {
+        wts = static_cast<double*>(base);
+        zsum = wts + kReconCover * Dx;
+        zsumf = reinterpret_cast<float*>(zsum + Dx);
+        offs = reinterpret_cast<uint32_t*>(zsumf + Dx);
+        ostr = offs + kReconCover * Dx;
+        cnt = ostr + kReconCover * Dx;
+    }
+};
+
+__global__ void __launch_bounds__(256) k_recon_table(const __grid_constant__ ReconParams p, void* table) {
+    const int Dx = static_cast<int>(p.D);
+    CovLayout t(table, Dx);
+    for (int x = threadIdx.x; x < Dx; x += blockDim.x) {
+        double zs = 0.0;
+        float zf = 0.f;
+        int c = 0;
+        for (int k = 0; k < p.n; ++k) {
+            const ReconEntry& e = p.e[k];
+            const int64_t j = x - e.begin;
+            if (j < 0 || j >= e.len) continue;
+            const double w = entry_weight(e, j);
+            zs = __dadd_rn(zs, w);
+            zf += static_cast<float>(w);
+            if (w != 0.0 && c < kReconCover) {
+                t.wts[c * Dx + x] = w;
+                t.offs[c * Dx + x] = static_cast<uint32_t>(e.base + j * p.inner);
+                t.ostr[c * Dx + x] = static_cast<uint32_t>(e.len * p.inner);
+                ++c;
+            }
+        }
+        t.zsum[x] = zs;
+        t.zsumf[x] = zf;
+        t.cnt[x] = static_cast<uint32_t>(c);
+    }
+}
+
+template <int D, bool UPDATE, bool FAST, bool VEC>
+__global__ void __launch_bounds__(256) k_reconstruct_cov(const __grid_constant__ ReconParams p,
+                                                         const typename Store<D>::T* __restrict__ preds,
+                                                         typename Store<D>::T* __restrict__ z,
+                                                         typename Store<D>::T* __restrict__ eps_out,
+                                                         const uint4* __restrict__ table, uint32_t table_vecs) {
+    using T = typename Store<D>::T;
+    extern __shared__ __align__(16) double cov[];
+    const int Dx = static_cast<int>(p.D);
+    for (uint32_t v = threadIdx.x; v < table_vecs; v += blockDim.x) reinterpret_cast<uint4*>(cov)[v] = __ldg(table + v);
+    const CovLayout t(cov, Dx);
+    const double* wts = t.wts;
+    const double* zsum = t.zsum;
+    const float* zsumf = t.zsumf;
+    const uint32_t* offs = t.offs;
+    const uint32_t* ostr = t.ostr;
+    const uint32_t* cnt = t.cnt;
+    const uint32_t inner = static_cast<uint32_t>(p.inner);
+    __syncthreads();
+    // one element: Σ_k w·pred (worker order) / Z, quantized; UPDATE: z - η ε̂, quantized
+    auto finish = [&](uint32_t x, uint32_t c, const T* r, T zraw, T& out) -> bool {
+        double eps;
+        if (!FAST) {
+            double a = 0.0;
+#pragma unroll
+            for (int cc = 0; cc < kReconCover; ++cc)
+                if (cc < c) a = __dadd_rn(a, __dmul_rn(wts[cc * Dx + x], load_val<D>(r, cc)));
+            const double Z = zsum[x];
+            eps = quantize_dev<D>(Z == 1.0 ? a : __ddiv_rn(a, Z));
+        } else {
+            float a = 0.f;
+#pragma unroll
+            for (int cc = 0; cc < kReconCover; ++cc)
+                if (cc < c) a = fmaf(static_cast<float>(wts[cc * Dx + x]), static_cast<float>(load_val<D>(r, cc)), a);
+            eps = quantize_dev<D>(static_cast<double>(a / zsumf[x]));
+        }
+        bool ok = isfinite(eps);
+        double res = eps;
+        if (UPDATE) {
+            const double zo = load_val<D>(&zraw, 0);
+            res = FAST ? static_cast<double>(fmaf(-static_cast<float>(p.eta), static_cast<float>(eps), static_cast<float>(zo)))
+                       : __dsub_rn(zo, __dmul_rn(p.eta, eps));
+        }
+        return store_q<D>(&out, 0, res) && ok;
+    };
+    constexpr int G = 8;  // elements per thread per iteration
+    const uint32_t total = static_cast<uint32_t>(p.total);
+    bool ok = true;
+    if (VEC) {
+        // 8 consecutive elements share (o, x): two 4-element vectors per covering prediction
+        for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < total / G; gi += gridDim.x * blockDim.x) {
+            const uint32_t idx0 = gi * G;
+            const uint32_t ox = fdiv(idx0, p.div_inner), i = idx0 - ox * inner;
+            const uint32_t o = fdiv(ox, p.div_d), x = ox - o * static_cast<uint32_t>(Dx);
+            const uint32_t c = cnt[x];
+            T raw[G][kReconCover];
+#pragma unroll
+            for (int cc = 0; cc < kReconCover; ++cc) {
+                if (cc < c) {
+                    const T* src = preds + offs[cc * Dx + x] + static_cast<uint64_t>(o) * ostr[cc * Dx + x] + i;
+#pragma unroll
+                    for (int h = 0; h < G / 4; ++h) {
+                        const typename Vec4<D>::T v = vload4<D>(src + 4 * h);
+                        const T* vt = reinterpret_cast<const T*>(&v);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) raw[4 * h + u][cc] = vt[u];
+                    }
+                }
+            }
+            T zr[G], q[G];
+            if (UPDATE) {
+#pragma unroll
+                for (int h = 0; h < G / 4; ++h)
+                    *reinterpret_cast<typename Vec4<D>::T*>(zr + 4 * h) = vload4<D>(z + idx0 + 4 * h);
+            }
+#pragma unroll
+            for (int u = 0; u < G; ++u) ok = finish(x, c, raw[u], UPDATE ? zr[u] : T{}, q[u]) && ok;
+            T* out = (UPDATE ? z : eps_out) + idx0;
+#pragma unroll
+            for (int h = 0; h < G / 4; ++h)
+                *reinterpret_cast<typename Vec4<D>::T*>(out + 4 * h) = *reinterpret_cast<const typename Vec4<D>::T*>(q + 4 * h);
+        }
+    } else {
+        // lane-strided: a warp owns 32*G consecutive elements, element u of a lane sits at
+        // +32u — every load and store instruction of the warp is one contiguous run
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+        for (uint32_t wc = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wc * (32u * G) < total; wc += warps) {
+            T raw[G][kReconCover], zr[G];
+            uint32_t xs[G], cs[G];
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                const uint32_t idx = wc * (32u * G) + 32u * u + lane;
+                cs[u] = 0;
+                xs[u] = 0;
+                if (idx < total) {
+                    const uint32_t ox = fdiv(idx, p.div_inner), i = idx - ox * inner;
+                    const uint32_t o = fdiv(ox, p.div_d), x = ox - o * static_cast<uint32_t>(Dx);
+                    const uint32_t c = cnt[x];
+                    xs[u] = x;
+                    cs[u] = c;
+#pragma unroll
+                    for (int cc = 0; cc < kReconCover; ++cc)
+                        if (cc < c) raw[u][cc] = preds[offs[cc * Dx + x] + static_cast<uint64_t>(o) * ostr[cc * Dx + x] + i];
+                    if (UPDATE) zr[u] = z[idx];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                const uint32_t idx = wc * (32u * G) + 32u * u + lane;
+                if (idx < total) {
+                    T qv;
+                    ok = finish(xs[u], cs[u], raw[u], UPDATE ? zr[u] : T{}, qv) && ok;
+                    (UPDATE ? z : eps_out)[idx] = qv;
+                }
+            }
+        }
+    }
+    if (!ok) raise_flag(LP_FLAG_NONFINITE);
+}
+
+// K10 for inner == 1 (W-axis plans): x-stationary.  A thread keeps one position x for its
+// whole life — grid threads are used in multiples of D, so thread g owns x = g % D and walks
+// rows o = g / D, g / D + R, ... (R = threads / D) — which puts its coverage-table column
+// (weights, offsets, Z) in registers, loaded once.  Lanes hold consecutive x, so every load and
+// store instruction of a warp is one contiguous run; 4 rows are in flight per iteration.
+template <int D, bool UPDATE, bool FAST>
+__global__ void __launch_bounds__(256) k_reconstruct_xs(const __grid_constant__ ReconParams p,
+                                                        const typename Store<D>::T* __restrict__ preds,
+                                                        typename Store<D>::T* __restrict__ z,
+                                                        typename Store<D>::T* __restrict__ eps_out,
+                                                        const void* __restrict__ table, uint32_t live) {
+    using T = typename Store<D>::T;
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= live) return;
+    const uint32_t Dx = static_cast<uint32_t>(p.D), rows = static_cast<uint32_t>(p.outer);
+    const uint32_t x = g % Dx, R = live / Dx;
+    const CovLayout t(const_cast<void*>(table), static_cast<int>(Dx));
+    const uint32_t c = __ldg(t.cnt + x);
+    double w[kReconCover];
+    uint32_t off[kReconCover], str[kReconCover];
+#pragma unroll
+    for (int cc = 0; cc < kReconCover; ++cc) {
+        w[cc] = cc < c ? __ldg(t.wts + cc * Dx + x) : 0.0;
+        off[cc] = cc < c ? __ldg(t.offs + cc * Dx + x) : 0u;
+        str[cc] = cc < c ? __ldg(t.ostr + cc * Dx + x) : 0u;
+    }
+    const double Z = __ldg(t.zsum + x);
+    const float Zf = __ldg(t.zsumf + x);
+    bool ok = true;
+    constexpr int U = 4;
+    for (uint32_t o0 = g / Dx; o0 < rows; o0 += U * R) {
+        T raw[U][kReconCover], zr[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t o = o0 + u * R;
+            if (o < rows) {
+#pragma unroll
+                for (int cc = 0; cc < kReconCover; ++cc)
+                    if (cc < c) raw[u][cc] = preds[off[cc] + static_cast<uint64_t>(o) * str[cc]];
+                if (UPDATE) zr[u] = z[static_cast<uint64_t>(o) * Dx + x];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t o = o0 + u * R;
+            if (o >= rows) continue;
+            double eps;
+            if (!FAST) {
+                double a = 0.0;
+#pragma unroll
+                for (int cc = 0; cc < kReconCover; ++cc)
+                    if (cc < c) a = __dadd_rn(a, __dmul_rn(w[cc], load_val<D>(raw[u], cc)));
+                eps = quantize_dev<D>(Z == 1.0 ? a : __ddiv_rn(a, Z));
+            } else {
+                float a = 0.f;
+#pragma unroll
+                for (int cc = 0; cc < kReconCover; ++cc)
+                    if (cc < c) a = fmaf(static_cast<float>(w[cc]), static_cast<float>(load_val<D>(raw[u], cc)), a);
+                eps = quantize_dev<D>(static_cast<double>(a / Zf));
+            }
+            ok = ok && isfinite(eps);
+            double res = eps;
+            if (UPDATE) {
+                const double zo = load_val<D>(zr, u);
+                res = FAST ? static_cast<double>(fmaf(-static_cast<float>(p.eta), static_cast<float>(eps), static_cast<float>(zo)))
+                           : __dsub_rn(zo, __dmul_rn(p.eta, eps));
+            }
+            ok = store_q<D>(UPDATE ? z : eps_out, static_cast<uint64_t>(o) * Dx + x, res) && ok;
+        }
+    }
+    if (!ok) raise_flag(LP_FLAG_NONFINITE);
+}
+
+// Coverage-table K10 applicability: 32-bit offsets, total % 4 == 0, every position covered
+// by at most kReconCover entries, table in 48 KB.  Returns the table bytes, 0 if not usable.
+static size_t recon_cov_bytes(const ReconParams& p, int dtype) {
+    if (!p.use32) return 0;
+    int64_t preds = 0;
+    for (int k = 0; k < p.n; ++k) preds += p.e[k].len * p.outer * p.inner;
+    if (preds >= (1ll << 31)) return 0;
+    for (int64_t x = 0; x < p.D; ++x) {
+        int c = 0;
+        for (int k = 0; k < p.n; ++k) c += (x >= p.e[k].begin && x < p.e[k].begin + p.e[k].len);
+        if (c > kReconCover) return 0;
+    }
+    (void)dtype;
+    const size_t bytes = (static_cast<size_t>(p.D) * (kReconCover * 8 + 8 + 4 + kReconCover * 8 + 4) + 15) / 16 * 16;
+    return bytes <= 48 * 1024 ? bytes : 0;
+}
+
+// Device coverage tables, cached per (device, plan entries, gather bases, D, inner).  Built on
+// first use (eagerly: the engine's first step of an axis precedes any graph capture).
+static const void* recon_table(const ReconParams& p, size_t bytes, cudaStream_t st) {
+    static std::mutex mu;
+    static std::map<std::string, void*> cache;
+    int dev = 0;
+    LP_CUDA(cudaGetDevice(&dev));
+    std::string key(reinterpret_cast<const char*>(&dev), sizeof(dev));
+    key.append(reinterpret_cast<const char*>(&p.D), sizeof(p.D));
+    key.append(reinterpret_cast<const char*>(&p.inner), sizeof(p.inner));
+    key.append(reinterpret_cast<const char*>(p.e), sizeof(ReconEntry) * static_cast<size_t>(p.n));
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    void* t = nullptr;
+    LP_CUDA(cudaMalloc(&t, bytes));
+    k_recon_table<<<1, 256, 0, st>>>(p, t);
+    LP_LAUNCH_CHECK();
+    cache.emplace(std::move(key), t);
+    return t;
+}
+
 template <int D, bool UPDATE>
 static void launch_recon(const ReconParams& p, const void* preds, void* z, void* eps, bool fast, cudaStream_t st) {
     using T = typename Store<D>::T;
     const int g = grid_for(p.total, 256);
     const size_t tab = sizeof(double) * static_cast<size_t>(p.n + 1) * static_cast<size_t>(p.D);
-    if (!fast && p.use32 && tab <= 48 * 1024) {
+    const size_t cov = tune_get("recon_cov", 1) ? recon_cov_bytes(p, D) : 0;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(preds) | reinterpret_cast<uintptr_t>(UPDATE ? z : eps);
+    if (cov) {
+        bool vec = p.inner % 8 == 0 && al % (4 * D) == 0;  // 8 elements share (o, x); prediction vectors need 8-aligned bases
+        for (int k = 0; k < p.n; ++k) vec = vec && p.e[k].base % 8 == 0;
+        // one wave of resident blocks: each block builds its table once
+        const void* table = recon_table(p, cov, st);
+        const uint32_t tv = static_cast<uint32_t>(cov / 16);
+        int res = 0;
+        auto kfn = fast ? (vec ? k_reconstruct_cov<D, UPDATE, true, true> : k_reconstruct_cov<D, UPDATE, true, false>)
+                        : (vec ? k_reconstruct_cov<D, UPDATE, false, true> : k_reconstruct_cov<D, UPDATE, false, false>);
+        LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, kfn, 256, cov));
+        res = std::max(1, res);
+        const int gq = grid_for(p.total / 8, 256, res);
+        auto* out_z = static_cast<T*>(z);
+        auto* out_e = static_cast<T*>(eps);
+        const auto* in = static_cast<const T*>(preds);
+        if (p.inner == 1 && tune_get("recon_xs", 1)) {
+            // x-stationary: threads in a multiple of D, one resident wave
+            int rx = 0;
+            LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rx, fast ? k_reconstruct_xs<D, UPDATE, true>
+                                                                              : k_reconstruct_xs<D, UPDATE, false>, 256, 0));
+            const int64_t cap = static_cast<int64_t>(grid_for(INT32_MAX, 256, std::max(1, rx))) * 256;
+            const int64_t want = std::min<int64_t>(cap, p.total);
+            const uint32_t live = static_cast<uint32_t>(std::max<int64_t>(p.D, want / p.D * p.D));
+            const int gx = static_cast<int>((live + 255) / 256);
+            if (fast) k_reconstruct_xs<D, UPDATE, true><<<gx, 256, 0, st>>>(p, in, out_z, out_e, table, live);
+            else k_reconstruct_xs<D, UPDATE, false><<<gx, 256, 0, st>>>(p, in, out_z, out_e, table, live);
+        } else if (fast) {
+            if (vec) k_reconstruct_cov<D, UPDATE, true, true><<<gq, 256, cov, st>>>(p, in, out_z, out_e, static_cast<const uint4*>(table), tv);
+            else k_reconstruct_cov<D, UPDATE, true, false><<<gq, 256, cov, st>>>(p, in, out_z, out_e, static_cast<const uint4*>(table), tv);
+        } else {
+            if (vec) k_reconstruct_cov<D, UPDATE, false, true><<<gq, 256, cov, st>>>(p, in, out_z, out_e, static_cast<const uint4*>(table), tv);
+            else k_reconstruct_cov<D, UPDATE, false, false><<<gq, 256, cov, st>>>(p, in, out_z, out_e, static_cast<const uint4*>(table), tv);
+        }
+    } else if (!fast && p.use32 && tab <= 48 * 1024) {
         k_reconstruct_tab<D, UPDATE><<<g, 256, tab, st>>>(p, static_cast<const T*>(preds), static_cast<T*>(z),
                                                           static_cast<T*>(eps));
     } else if (fast)
@@ -558,13 +1012,9 @@ int lp_extract(const lp_plan* plan, int32_t first, int32_t count, const void* z,
             fail(LP_ERR_SHAPE_MISMATCH, "plan was built for extent " + std::to_string(plan->axis_extent) +
                                             ", tensor has " + std::to_string(s.extent(plan->axis)));
         if (first < 0 || count < 0 || first + count > plan->n_entries) fail(LP_ERR_OUT_OF_BOUNDS, "entry range");
-        const auto n = entry_elems(*plan, s);
-        char* d = static_cast<char*>(dst);
-        for (int k = first; k < first + count; ++k) {
-            slice_to(z, s, plan->axis, plan->entries[k].latent_begin, plan->entries[k].latent_end, dtype, d,
-                     as_stream(stream));
-            d += n[k] * dtype;
-        }
+        std::vector<int> ks(count);
+        for (int c = 0; c < count; ++c) ks[c] = first + c;
+        gather_entries(z, s, *plan, ks.data(), count, dtype, dst, as_stream(stream));  // K1, one launch
     });
 }
 

@@ -34,5 +34,8 @@ ReconParams make_recon_params(const lp_plan& plan, const Shape4& s, const std::v
 void reconstruct_dispatch(const ReconParams& p, int dtype, const void* preds, void* z, void* eps, bool update,
                           bool fast, cudaStream_t st);
 void slice_to(const void* z, const Shape4& s, int axis, i64 begin, i64 end, int E, void* dst, cudaStream_t st);
+// K1 for several entries of one plan in one launch, packed in the order of ks.
+void gather_entries(const void* z, const Shape4& s, const lp_plan& plan, const int* ks, int count, int E, void* dst,
+                    cudaStream_t st);
 
 }  // namespace lpb200

@@ -1,0 +1,87 @@
+"""K1 (partition gather) and K10 (reconstruct + sampler update) micro-benchmark at the BASELINE
+latent sizes: per-launch device time (CUDA events, L2 flushed before every launch so inputs
+come from HBM), achieved algorithmic GB/s and fraction of the measured HBM copy bandwidth.
+
+Algorithmic bytes: K1 = 2 * shard elements * b; K10 = (sum of shard elements +
+2 * latent elements) * b (every prediction read once, z read and written).
+
+usage: python scripts/hbm_bench.py [dtype_bytes=4]  ->  gpurun_out/hbm_bench.json
+"""
+import ctypes as C
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2512_07350_b200 import _lib, lp  # noqa: E402
+
+L = _lib.lib()
+PEAK = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6452.5
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+st = lambda: C.c_void_p(torch.cuda.current_stream().cuda_stream)  # noqa: E731
+DT = {2: torch.int16, 4: torch.float32, 8: torch.float64}
+
+
+def timed(fn, reps=20):
+    fn()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def case(name, dims, K, r, d):
+    out = []
+    n = 1
+    for x in dims:
+        n *= x
+    z = torch.randn(n, device="cuda").to(DT[d]) if d != 2 else torch.randint(0, 0x3b00, (n,), device="cuda", dtype=torch.int16)
+    for step, axis in ((1, "T"), (2, "H"), (3, "W")):
+        plan = lp.build_plan(dims, (1, 2, 2), step, K, r)
+        subs = [plan.sub_shape(dims, k) for k in range(plan.workers)]
+        vols = [s[0] * s[1] * s[2] * s[3] for s in subs]
+        packed = torch.empty(sum(vols), device="cuda", dtype=DT[d])
+        if d == 2:
+            packed.copy_(torch.randint(0, 0x3b00, (sum(vols),), device="cuda", dtype=torch.int16))
+        else:
+            packed.normal_()
+        shape = _lib.i64arr(dims)
+        # K1: gather every entry (one launch for all entries, as the engine does for its owned run)
+        k1 = timed(lambda: _lib.check(L.lp_extract(C.byref(plan.raw), 0, plan.workers, C.c_void_p(z.data_ptr()), shape, d,
+                                                   C.c_void_p(packed.data_ptr()), st())))
+        k1_bytes = 2.0 * sum(vols) * d
+        k10 = timed(lambda: _lib.check(L.lp_reconstruct_update(C.byref(plan.raw), C.c_void_p(packed.data_ptr()), shape, d, 0,
+                                                              C.c_double(1e-30), C.c_void_p(z.data_ptr()), st())))
+        k10_bytes = (sum(vols) + 2.0 * n) * d
+        k10f = timed(lambda: _lib.check(L.lp_reconstruct_update(C.byref(plan.raw), C.c_void_p(packed.data_ptr()), shape, d, 1,
+                                                               C.c_double(1e-30), C.c_void_p(z.data_ptr()), st())))
+        row = {"config": name, "axis": axis, "K": K, "dtype_bytes": d, "latent_elems": n, "shard_elems": sum(vols),
+               "k1_us": k1 * 1e3, "k1_GBps": k1_bytes / k1 / 1e6, "k1_frac": k1_bytes / k1 / 1e6 / PEAK,
+               "k10_us": k10 * 1e3, "k10_GBps": k10_bytes / k10 / 1e6, "k10_frac": k10_bytes / k10 / 1e6 / PEAK,
+               "k10_fast_us": k10f * 1e3, "k10_fast_frac": k10_bytes / k10f / 1e6 / PEAK}
+        print(json.dumps(row), flush=True)
+        out.append(row)
+    return out
+
+
+def main():
+    d = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+    rows = []
+    rows += case("C2", (16, 21, 60, 104), 4, 0.5, d)
+    rows += case("C4", (16, 21, 90, 160), 8, 0.5, d)
+    rows += case("C5", (16, 41, 60, 104), 8, 0.5, d)
+    tag = os.environ.get("HB_TAG", "")
+    json.dump({"peak_GBps": PEAK, "rows": rows}, open(f"gpurun_out/hbm_bench{tag}.json", "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -231,7 +231,10 @@ def run_ours(args, rank, world, local_rank):
     L = _lib.lib()
     torch.cuda.set_device(local_rank)
     _lib.check(L.lp_device_check(local_rank))
-    K = args.workers or max(4, world)
+    M = max(1, args.hybrid)
+    if world % M:
+        raise SystemExit(f"--hybrid {M} must divide the number of GPUs {world}")
+    K = args.workers or (world // M if M > 1 else max(4, world))
     z_host_np, cond = lp.synthetic_latent_host(DIMS, 4, SEED)
     dit = lp.DiTDenoiser(cond, num_layers=args.layers)
     nccl_id = None
@@ -240,7 +243,7 @@ def run_ours(args, rank, world, local_rank):
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     eng = lp.LpEngine(DIMS, PATCH, 4, K, R_OVERLAP, T_SCHED, ETA, W_CFG, cond, denoiser="dit", dit=dit, world=world,
-                      rank=rank, nccl_id=nccl_id)
+                      rank=rank, nccl_id=nccl_id, group_size=M)
     z0 = torch.from_numpy(z_host_np.astype("float32")).pin_memory()
     eng.z.data.copy_(z0)
     stream = torch.cuda.current_stream()
@@ -359,12 +362,12 @@ def run_ours(args, rank, world, local_rank):
     step_tflops = step_flops / (ms / args.steps / 1000.0) / 1e12
     # communication per video (50 steps): measured NCCL bytes, exact all-gather layout, reference ledger, NMP
     per_step_nccl = (c1["nccl_bytes_received"] - c0["nccl_bytes_received"]) * world / args.steps
-    led = ag = 0
+    led = ag_video = 0
     for i in range(1, T_SCHED + 1):
         p = lp.build_plan(DIMS, PATCH, i, K, R_OVERLAP)
-        a, b = lp.step_comm_bytes(p, DIMS, 2, world, 4)
+        a, b = lp.step_comm_bytes(p, DIMS, 2, world // M, 4)
         led += a
-        ag += b
+        ag_video += b
     tokens = (DIMS[1] // PATCH[0]) * (DIMS[2] // PATCH[1]) * (DIMS[3] // PATCH[2])
     nmp = 2 * T_SCHED * (K - 1) * tokens * 1536 * 2
     value = args.steps / (ms / 1000.0)
@@ -388,9 +391,17 @@ def run_ours(args, rank, world, local_rank):
         "allgather": ag,
         "clocks": clk.summary(),
         "comm": {"nccl_bytes_per_step_measured_all_ranks": per_step_nccl,
-                 "allgather_bytes_per_video": ag, "reference_ledger_bytes_per_video": led,
+                 "allgather_bytes_per_video": ag_video, "reference_ledger_bytes_per_video": led,
                  "reference_nmp_bytes_per_video": nmp, "wire": "f32 eps shards (ledger counts the 2-B preset width)"},
     }
+    if M > 1:
+        hy = eng.hybrid()
+        cr = lp.cost_report(T_SCHED, world, R_OVERLAP, DIMS, PATCH, preset="custom", hidden_dim=dit.cfg.dim,
+                            wire_bytes=4, hybrid=(world // M, [M] * (world // M)))
+        line["config"]["parallelism"] = f"hybrid: {world // M} LP groups x {M} pipeline stages"
+        line["hybrid"] = {"group_size": M, "groups": world // M, "rank0_layers": [hy["layer_begin"], hy["layer_end"]],
+                          "reference_cost_hybrid_intra_bytes_per_video_fp32": cr["hybrid"]["C_intra_total"],
+                          "reference_cost_hybrid_bound": cr["hybrid"]["bound"]}
     if world == 1 and not args.no_cpu_baseline:
         from oracle.oracle import reference_available
 
@@ -415,6 +426,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workers", type=int, default=0, help="LP workers K (default max(4, N))")
     ap.add_argument("--layers", type=int, default=30)
+    ap.add_argument("--hybrid", type=int, default=1,
+                    help="M > 1: hybrid LP x model parallelism, N/M LP groups of M pipeline stages (K = N/M)")
     ap.add_argument("--overlap", type=float, default=None,
                     help="LP overlap ratio r (BASELINE configs[2] sweep; default 0.5 = configs[1])")
     ap.add_argument("--cpu-steps", type=int, default=24)

@@ -275,6 +275,7 @@ void lp_dit_default_config(lp_dit_config* cfg); /* WAN2.1-1.3B shape */
  * device, initialised from the pinned generator (see lp_dit_param). */
 int lp_dit_create(const lp_dit_config* cfg, const double* cond_values, int32_t n_cond, lp_dit** out);
 int lp_dit_destroy(lp_dit* dit);
+int lp_dit_get_config(const lp_dit* dit, lp_dit_config* cfg_out);
 /* Workspace for shards up to max_tokens tokens (allocates; call once). */
 int lp_dit_reserve(lp_dit* dit, int64_t max_tokens);
 /* Independent workspaces ("slots") so that several shards' forwards can be in
@@ -282,6 +283,18 @@ int lp_dit_reserve(lp_dit* dit, int64_t max_tokens);
 int lp_dit_reserve_slots(lp_dit* dit, int64_t max_tokens, int32_t nslots);
 int lp_dit_cfg_predict_slot(lp_dit* dit, int32_t slot, const void* sub, const int64_t shape[4], int dtype_bytes,
                             int timestep, double guidance, void* eps_out, void* stream);
+/* Pipeline stage of the same forward (hybrid LP x intra-group model parallelism,
+ * src/cost.cpp:133-213 models its traffic): blocks [layer_begin, layer_end).  layer_begin == 0
+ * embeds `sub`; otherwise the slot's activation must hold the residual stream after block
+ * layer_begin-1.  layer_end == num_layers runs the head and writes ε̂ (eps_out); otherwise
+ * the activation is left for the next stage.  Stages chained over any split give the
+ * bit-identical ε̂ of lp_dit_cfg_predict_slot. */
+int lp_dit_forward_layers(lp_dit* dit, int32_t slot, const void* sub, const int64_t shape[4], int dtype_bytes,
+                          int timestep, double guidance, int32_t layer_begin, int32_t layer_end, void* eps_out,
+                          void* stream);
+/* The slot's activation (fp32 residual stream [2 * tokens, dim]) for a shard of `shape`:
+ * what one pipeline stage hands the next (bytes = 2 * tokens * dim * 4). */
+int lp_dit_activation(lp_dit* dit, int32_t slot, const int64_t shape[4], void** x_dptr, int64_t* bytes);
 /* cfg_predict with the DiT: CFG batch 2 (uncond = null text, cond = synthetic
  * text), one forward, combine uncond + w*(cond-uncond), quantize to dtype. */
 int lp_dit_cfg_predict(lp_dit* dit, const void* sub, const int64_t shape[4], int dtype_bytes, int timestep,
@@ -332,6 +345,12 @@ typedef struct lp_engine_config {
      * schedule[(i-1) % schedule_len].  Plans per axis are build_axis_plan's. */
     int32_t schedule_len;
     int32_t schedule[64];
+    /* Hybrid LP x intra-group model parallelism (src/cost.cpp:133-213):
+     * group_size M > 1 splits the world into world/M LP groups of M ranks; rank r is
+     * stage r % M of group r / M, running DiT blocks [s*L/M, (s+1)*L/M) and handing the
+     * activation to the next stage (ncclSend/Recv).  Entries are assigned to groups.  0 or 1
+     * = plain LP.  Requires the DiT denoiser. */
+    int32_t group_size;
 } lp_engine_config;
 
 typedef struct lp_engine lp_engine;
@@ -352,6 +371,19 @@ int lp_engine_run(lp_engine* e, int32_t first_step, int32_t count, void* stream)
  * between phases 1 and 3 (world slots of slot_elems elements, rank r's slot at r*slot_elems). */
 int lp_engine_step_phase(lp_engine* e, int32_t step, int32_t phase, void* stream);
 int lp_engine_gather_buffer(const lp_engine* e, int32_t step, void** buffer, int64_t* slot_elems);
+/* Hybrid engines (group_size M > 1), driven stage by stage without NCCL: runs this rank's
+ * pipeline stage for the idx-th entry its group owns at `step` (idx < lp_engine_owned).
+ * Stage 0 gathers (K1) and embeds; stages > 0 expect the previous stage's activation in
+ * lp_engine_stage_activation's buffer; the last stage writes ε̂ into its group's slot of the
+ * gather buffer (groups slots of slot_elems).  With NCCL, phase 1 runs every entry and the
+ * activations move by ncclSend/Recv; phase 2 broadcasts each group's slot from its last
+ * stage. */
+int lp_engine_stage(lp_engine* e, int32_t step, int32_t idx, void* stream);
+int lp_engine_stage_activation(lp_engine* e, int32_t step, int32_t idx, void** x_dptr, int64_t* bytes);
+int lp_engine_owned(const lp_engine* e, int32_t step, int32_t* n_owned);
+/* Group decomposition of this rank and the activation bytes it handed to the next stage. */
+int lp_engine_hybrid(const lp_engine* e, int32_t* group_size, int32_t* group, int32_t* stage, int32_t* layer_begin,
+                     int32_t* layer_end, uint64_t* intra_bytes);
 /* Bytes this engine moved over NCCL so far, and the reference ledger bytes. */
 int lp_engine_comm(const lp_engine* e, uint64_t* nccl_bytes, uint64_t* ledger_bytes);
 /* Kernel launches issued by the engine so far (this library's kernels only). */

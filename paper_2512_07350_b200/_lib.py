@@ -57,7 +57,7 @@ class EngineConfig(C.Structure):
                 ("mode", C.c_int32), ("eta", C.c_double), ("guidance", C.c_double), ("denoiser", C.c_int32),
                 ("wire_bytes", C.c_int32), ("radius", C.c_int64 * 3), ("t_coeff", C.c_double),
                 ("cond_coeff", C.c_double), ("world", C.c_int32), ("rank", C.c_int32), ("dit", C.c_void_p),
-                ("schedule_len", C.c_int32), ("schedule", C.c_int32 * 64)]
+                ("schedule_len", C.c_int32), ("schedule", C.c_int32 * 64), ("group_size", C.c_int32)]
 
 
 class CostReport(C.Structure):
@@ -128,6 +128,14 @@ _SIGS = {
     "lp_dit_time_on_device": (_i, [_vp, _i32]),
     "lp_engine_step_phase": (_i, [_vp, _i32, _i32, _vp]),
     "lp_engine_gather_buffer": (_i, [_vp, _i32, C.POINTER(_vp), C.POINTER(_i64)]),
+    "lp_engine_stage": (_i, [_vp, _i32, _i32, _vp]),
+    "lp_engine_stage_activation": (_i, [_vp, _i32, _i32, C.POINTER(_vp), C.POINTER(_i64)]),
+    "lp_engine_owned": (_i, [_vp, _i32, C.POINTER(_i32)]),
+    "lp_engine_hybrid": (_i, [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32),
+                              C.POINTER(_i32), C.POINTER(C.c_uint64)]),
+    "lp_dit_forward_layers": (_i, [_vp, _i32, _vp, _i64p, _i, _i, _d, _i32, _i32, _vp, _vp]),
+    "lp_dit_activation": (_i, [_vp, _i32, _i64p, C.POINTER(_vp), C.POINTER(_i64)]),
+    "lp_dit_get_config": (_i, [_vp, _vp]),
     "lp_verify_n_complete": (_i, [_i64p, _i32, _d, C.POINTER(_i32), _i32, _i32, _i64, C.POINTER(_i32),
                                   C.POINTER(_i32), _i64p, C.POINTER(_i32)]),
     "lp_coverage_trace": (_i, [_i64p, _i32, _d, C.POINTER(_i32), _i32, _i32, _i64, _i64p, _f64p, C.POINTER(_i32)]),

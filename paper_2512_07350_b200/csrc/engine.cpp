@@ -48,6 +48,10 @@ struct lp_engine {
     cudaEvent_t ev_fork = nullptr, ev_join[4] = {};
     ncclComm_t comm = nullptr;
     uint64_t nccl_bytes = 0, ledger_bytes = 0, launches = 0;
+    // hybrid LP x model-parallel groups (group_size M > 1): this rank is pipeline stage
+    // `stage` of LP group `group`, running DiT blocks [layer0, layer1)
+    int M = 1, groups = 1, group = 0, stage = 0, layer0 = 0, layer1 = 0;
+    uint64_t intra_bytes = 0;  // activation bytes this rank sent to the next stage
     // DiT engines replay each axis's step as a CUDA graph (captured the second time the
     // axis comes up, so every kernel's one-time setup has run eagerly first)
     cudaGraphExec_t graph[3] = {};
@@ -82,6 +86,24 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
             if (c->schedule[i] < 0 || c->schedule[i] > 2) fail(LP_ERR_INVALID_ARGUMENT, "schedule axes must be 0..2");
         auto* e = new lp_engine();
         e->cfg = *c;
+        e->M = c->group_size > 1 ? c->group_size : 1;
+        e->groups = c->world;  // plain LP: every rank is its own group
+        if (e->M > 1) {
+            if (!c->dit) { delete e; fail(LP_ERR_INVALID_GROUPING, "hybrid groups need the DiT denoiser"); }
+            if (c->world % e->M) { delete e; fail(LP_ERR_INVALID_GROUPING, "world must be a multiple of group_size"); }
+            int L = 0;
+            {
+                lp_dit_config dc;
+                lp_dit_get_config(c->dit, &dc);
+                L = dc.num_layers;
+            }
+            if (e->M > L) { delete e; fail(LP_ERR_INVALID_GROUPING, "more pipeline stages than DiT blocks"); }
+            e->groups = c->world / e->M;
+            e->group = c->rank / e->M;
+            e->stage = c->rank % e->M;
+            e->layer0 = static_cast<int>(static_cast<int64_t>(e->stage) * L / e->M);
+            e->layer1 = static_cast<int>(static_cast<int64_t>(e->stage + 1) * L / e->M);
+        }
         e->shape = Shape4::from(c->shape);
         e->cond.assign(cond, cond + n_cond);
         if (n_cond > 0) {  // ConditioningVector::mean (src/denoise.cpp:17-22)
@@ -94,7 +116,7 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
             for (int a = 0; a < 3; ++a) {
                 // step index a+1 has axis a; step_index is cosmetic in the plan
                 e->plans[a] = build_plan_for_shape(e->shape, c->patch, a + 1, c->workers, c->overlap_ratio);
-                e->layout[a] = shard_layout(e->plans[a], e->shape, c->world, c->rank);
+                e->layout[a] = shard_layout(e->plans[a], e->shape, e->groups, e->M > 1 ? e->group : c->rank);
                 e->elems[a] = entry_elems(e->plans[a], e->shape);
                 e->recon[a] = make_recon_params(e->plans[a], e->shape, e->layout[a].base, c->eta);
                 max_slot = std::max(max_slot, e->layout[a].slot_elems);
@@ -102,12 +124,12 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
             }
             const size_t E = static_cast<size_t>(c->dtype_bytes);
             LP_CUDA(cudaMalloc(&e->z, static_cast<size_t>(e->shape.volume()) * E));
-            LP_CUDA(cudaMalloc(&e->gather, static_cast<size_t>(max_slot) * c->world * E));
-            LP_CUDA(cudaMemset(e->gather, 0, static_cast<size_t>(max_slot) * c->world * E));
+            LP_CUDA(cudaMalloc(&e->gather, static_cast<size_t>(max_slot) * e->groups * E));
+            LP_CUDA(cudaMemset(e->gather, 0, static_cast<size_t>(max_slot) * e->groups * E));
             size_t max_owned = 1;
             for (int a = 0; a < 3; ++a) max_owned = std::max(max_owned, e->layout[a].owned.size());
             const int want_slots = std::max(1, std::min(4, tune_get("engine_slots", 2)));
-            if (c->dit && max_owned > 1) e->nslots = static_cast<int>(std::min<size_t>(max_owned, want_slots));
+            if (c->dit && max_owned > 1 && e->M == 1) e->nslots = static_cast<int>(std::min<size_t>(max_owned, want_slots));
             // K1 gathers every owned entry of a step in one launch, packed in owned order
             size_t max_owned_elems = 1;
             for (int a = 0; a < 3; ++a) {
@@ -190,7 +212,14 @@ int step_axis(const lp_engine* e, int i) {
 // Phase 1 of step i (run_lp body, src/cluster.cpp:178-206): K1 + cfg_predict for every entry
 // this rank owns, written into its slot of the gather buffer (owned shards overlap on the
 // slot streams when there are several).
+void hybrid_entry(lp_engine* e, int i, int idx, cudaStream_t st);
+
 void step_compute(lp_engine* e, int i, cudaStream_t st) {
+    if (e->M > 1) {
+        const int n = static_cast<int>(e->layout[step_axis(e, i)].owned.size());
+        for (int idx = 0; idx < n; ++idx) hybrid_entry(e, i, idx, st);
+        return;
+    }
     const lp_engine_config& c = e->cfg;
     const int E = c.dtype_bytes;
     char* gather = static_cast<char*>(e->gather);
@@ -234,6 +263,45 @@ void step_compute(lp_engine* e, int i, cudaStream_t st) {
     }
 }
 
+// Hybrid LP x model-parallel groups: this rank's pipeline stage for the idx-th entry its
+// group owns at step i.  Stage 0 gathers the group's entries (one K1 launch, at idx 0) and
+// embeds; every stage runs its blocks; stages > 0 first receive the activation from rank-1,
+// stages < M-1 send it to rank+1 afterwards (NCCL; without a communicator the caller moves
+// it, lp_engine_stage_activation); the last stage writes ε̂ into the group's gather slot.
+void hybrid_entry(lp_engine* e, int i, int idx, cudaStream_t st) {
+    const lp_engine_config& c = e->cfg;
+    const int E = c.dtype_bytes, t = c.total_steps + 1 - i, a = step_axis(e, i);
+    const lp_plan& plan = e->plans[a];
+    const ShardLayout& L = e->layout[a];
+    if (idx < 0 || idx >= static_cast<int>(L.owned.size())) fail(LP_ERR_OUT_OF_BOUNDS, "owned entry index");
+    if (e->stage == 0 && idx == 0)
+        gather_entries(e->z, e->shape, plan, L.owned.data(), static_cast<int>(L.owned.size()), E, e->sub, st);  // K1
+    size_t sub_off = 0;
+    for (int j = 0; j < idx; ++j) sub_off += static_cast<size_t>(e->elems[a][L.owned[j]]) * E;
+    const int k = L.owned[idx];
+    const lp_entry& en = plan.entries[k];
+    const Shape4 s = e->shape.with_extent(a, en.latent_end - en.latent_begin);
+    const int64_t sh[4] = {s.c, s.t, s.h, s.w};
+    void* x = nullptr;
+    int64_t xb = 0;
+    int rc = lp_dit_activation(c.dit, 0, sh, &x, &xb);
+    if (rc) fail(rc, lp_last_error());
+    if (e->stage > 0 && e->comm) {
+        LP_NCCL(ncclRecv(x, static_cast<size_t>(xb), ncclUint8, c.rank - 1, e->comm, st));
+        e->nccl_bytes += static_cast<uint64_t>(xb);
+    }
+    void* eps = static_cast<char*>(e->gather) + static_cast<size_t>(L.base[k]) * E;
+    rc = lp_dit_forward_layers(c.dit, 0, e->stage == 0 ? static_cast<char*>(e->sub) + sub_off : nullptr, sh, E, t,
+                               c.guidance, e->layer0, e->layer1, eps, st);
+    if (rc)
+        fail(LP_ERR_WORKER_FAILURE,
+             "worker " + std::to_string(k + 1) + " failed at step " + std::to_string(i) + ": " + lp_last_error());
+    if (e->stage < e->M - 1) {
+        if (e->comm) LP_NCCL(ncclSend(x, static_cast<size_t>(xb), ncclUint8, c.rank + 1, e->comm, st));
+        e->intra_bytes += static_cast<uint64_t>(xb);
+    }
+}
+
 // Phase 2 (K9): one in-place ncclAllGather of the padded rank slots.
 void step_exchange(lp_engine* e, int i, cudaStream_t st) {
     const lp_engine_config& c = e->cfg;
@@ -241,8 +309,16 @@ void step_exchange(lp_engine* e, int i, cudaStream_t st) {
     const size_t slot = static_cast<size_t>(L.slot_elems) * c.dtype_bytes;
     char* gather = static_cast<char*>(e->gather);
     prof_begin(KC_ALLGATHER, st);
-    LP_NCCL(ncclAllGather(gather + slot * c.rank, gather, slot, ncclUint8, e->comm, st));
-    prof_end(KC_ALLGATHER, st, 0.0, static_cast<double>(slot) * (c.world - 1));
+    if (e->M == 1) {
+        LP_NCCL(ncclAllGather(gather + slot * c.rank, gather, slot, ncclUint8, e->comm, st));
+    } else {
+        // hybrid: group g's ε̂ slot lives on its last stage (rank g*M + M-1)
+        LP_NCCL(ncclGroupStart());
+        for (int g = 0; g < e->groups; ++g)
+            LP_NCCL(ncclBroadcast(gather + slot * g, gather + slot * g, slot, ncclUint8, g * e->M + e->M - 1, e->comm, st));
+        LP_NCCL(ncclGroupEnd());
+    }
+    prof_end(KC_ALLGATHER, st, 0.0, static_cast<double>(slot) * (e->groups - 1));
 }
 
 // Phase 3 (K10): reconstruct + sampler update of the replicated z from the gathered shards,
@@ -258,7 +334,10 @@ void step_reconstruct(lp_engine* e, int i, cudaStream_t st) {
 void account_step(lp_engine* e, int i) {
     const lp_engine_config& c = e->cfg;
     const int a = step_axis(e, i);
-    if (e->comm) e->nccl_bytes += static_cast<size_t>(e->layout[a].slot_elems) * c.dtype_bytes * (c.world - 1);
+    if (e->comm) {
+        const int foreign = e->M == 1 ? c.world - 1 : e->groups - (e->stage == e->M - 1 ? 1 : 0);
+        e->nccl_bytes += static_cast<size_t>(e->layout[a].slot_elems) * c.dtype_bytes * foreign;
+    }
     uint64_t sum = 0;
     for (size_t k = 1; k < e->elems[a].size(); ++k) sum += static_cast<uint64_t>(e->elems[a][k]);
     e->ledger_bytes += 4ull * sum * static_cast<uint64_t>(c.wire_bytes);
@@ -351,6 +430,44 @@ int lp_engine_step_phase(lp_engine* e, int32_t step, int32_t phase, void* stream
         else fail(LP_ERR_INVALID_ARGUMENT, "phase must be 1 (compute), 2 (exchange) or 3 (reconstruct)");
         e->launches += launch_count() - l0;
     });
+}
+
+int lp_engine_stage(lp_engine* e, int32_t step, int32_t idx, void* stream) {
+    return guard([&] {
+        if (e->M < 2) fail(LP_ERR_INVALID_GROUPING, "lp_engine_stage needs group_size > 1");
+        const uint64_t l0 = launch_count();
+        hybrid_entry(e, step, idx, as_stream(stream));
+        e->launches += launch_count() - l0;
+    });
+}
+
+int lp_engine_stage_activation(lp_engine* e, int32_t step, int32_t idx, void** x, int64_t* bytes) {
+    return guard([&] {
+        const int a = step_axis(e, step);
+        const ShardLayout& L = e->layout[a];
+        if (idx < 0 || idx >= static_cast<int>(L.owned.size())) fail(LP_ERR_OUT_OF_BOUNDS, "owned entry index");
+        const lp_entry& en = e->plans[a].entries[L.owned[idx]];
+        const Shape4 s = e->shape.with_extent(a, en.latent_end - en.latent_begin);
+        const int64_t sh[4] = {s.c, s.t, s.h, s.w};
+        const int rc = lp_dit_activation(e->cfg.dit, 0, sh, x, bytes);
+        if (rc) fail(rc, lp_last_error());
+    });
+}
+
+int lp_engine_hybrid(const lp_engine* e, int32_t* group_size, int32_t* group, int32_t* stage, int32_t* layer_begin,
+                     int32_t* layer_end, uint64_t* intra_bytes) {
+    *group_size = e->M;
+    *group = e->group;
+    *stage = e->stage;
+    *layer_begin = e->layer0;
+    *layer_end = e->layer1;
+    *intra_bytes = e->intra_bytes;
+    return LP_OK;
+}
+
+int lp_engine_owned(const lp_engine* e, int32_t step, int32_t* n_owned) {
+    *n_owned = static_cast<int32_t>(e->layout[step_axis(e, step)].owned.size());
+    return LP_OK;
 }
 
 int lp_engine_gather_buffer(const lp_engine* e, int32_t step, void** buffer, int64_t* slot_elems) {

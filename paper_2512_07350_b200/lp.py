@@ -466,7 +466,7 @@ class LpEngine:
 
     def __init__(self, dims, patch, dtype_bytes, workers, overlap_ratio, steps, eta, guidance, cond,
                  denoiser="box", radius=(1, 1, 1), wire_bytes=2, world=1, rank=0, nccl_id=None, mode="exact",
-                 dit: DiTDenoiser | None = None, t_coeff=0.01, cond_coeff=0.1, schedule=None):
+                 dit: DiTDenoiser | None = None, t_coeff=0.01, cond_coeff=0.1, schedule=None, group_size=1):
         cfg = _lib.EngineConfig()
         for i in range(4):
             cfg.shape[i] = int(dims[i])
@@ -490,6 +490,7 @@ class LpEngine:
         cfg.world = world
         cfg.rank = rank
         cfg.dit = dit.handle if dit is not None else None
+        cfg.group_size = int(group_size)
         if schedule:
             axes = parse_schedule(schedule)
             cfg.schedule_len = len(axes)
@@ -497,6 +498,8 @@ class LpEngine:
                 cfg.schedule[i] = a
         self.dit = dit
         self.world = int(world)
+        self.group_size = max(1, int(group_size))
+        self.groups = self.world // self.group_size
         self.dims = tuple(int(d) for d in dims)
         self.dtype_bytes = dtype_bytes
         c = (C.c_double * len(cond))(*cond)
@@ -529,7 +532,33 @@ class LpEngine:
         check(lib().lp_engine_gather_buffer(self.handle, int(step), C.byref(ptr), C.byref(slot)))
         torch = _torch()
         dt = getattr(torch, _TORCH_DT[self.dtype_bytes])
-        return _wrap_device(ptr.value, self.world * slot.value, dt), slot.value
+        return _wrap_device(ptr.value, self.groups * slot.value, dt), slot.value
+
+    # --- hybrid LP x model-parallel groups (group_size > 1), SURVEY.md §8 f2 ---
+    def owned(self, step):
+        n = C.c_int32()
+        check(lib().lp_engine_owned(self.handle, int(step), C.byref(n)))
+        return int(n.value)
+
+    def stage(self, step, idx, stream=None):
+        """This rank's pipeline stage for the idx-th entry its group owns (no-NCCL driving)."""
+        st = C.c_void_p(stream) if stream is not None else _stream()
+        check(lib().lp_engine_stage(self.handle, int(step), int(idx), st))
+
+    def stage_activation(self, step, idx):
+        """torch float32 view of the activation handed between stages for that entry."""
+        ptr, nb = C.c_void_p(), C.c_int64()
+        check(lib().lp_engine_stage_activation(self.handle, int(step), int(idx), C.byref(ptr), C.byref(nb)))
+        return _wrap_device(ptr.value, nb.value // 4, _torch().float32)
+
+    def hybrid(self):
+        v = [C.c_int32() for _ in range(5)]
+        intra = C.c_uint64()
+        check(lib().lp_engine_hybrid(self.handle, *[C.byref(x) for x in v], C.byref(intra)))
+        keys = ("group_size", "group", "stage", "layer_begin", "layer_end")
+        out = {k: int(x.value) for k, x in zip(keys, v)}
+        out["intra_bytes_sent"] = int(intra.value)
+        return out
 
     def comm(self):
         a, b = C.c_uint64(), C.c_uint64()

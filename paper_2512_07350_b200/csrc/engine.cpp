@@ -420,7 +420,11 @@ int lp_engine_step_phase(lp_engine* e, int32_t step, int32_t phase, void* stream
     return guard([&] {
         cudaStream_t st = as_stream(stream);
         const uint64_t l0 = launch_count();
-        if (phase == 1) step_compute(e, step, st);
+        if (phase == 1) {
+            if (e->M > 1 && !e->comm)
+                fail(LP_ERR_INVALID_GROUPING, "hybrid engine without NCCL: drive its stages with lp_engine_stage");
+            step_compute(e, step, st);
+        }
         else if (phase == 2) {
             if (e->comm) step_exchange(e, step, st);
         } else if (phase == 3) {

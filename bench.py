@@ -38,6 +38,12 @@ METRIC = "LP denoise steps/s, WAN-1.3B-shape 480p 81f (C2)"
 UNIT = "steps/s"
 
 
+# LP_BENCH_GLOO_TEST=1 (torchrun on a ONE-GPU box): every rank on GPU 0, gloo plumbing, no
+# NCCL communicator, ε̂ exchange over CUDA IPC peer memory.  Validates the multi-rank bench
+# path where NCCL refuses two ranks on one device; its numbers are not scaling numbers.
+GLOO_TEST = os.environ.get("LP_BENCH_GLOO_TEST") == "1"
+
+
 def workload(K, world, layers):
     return {
         "workload": f"C2: WAN2.1-1.3B-shaped DiT ({layers} blocks, d=1536, 12 heads, ffn 8960, CFG batch 2) on 480p81f "
@@ -238,12 +244,29 @@ def run_ours(args, rank, world, local_rank):
     z_host_np, cond = lp.synthetic_latent_host(DIMS, 4, SEED)
     dit = lp.DiTDenoiser(cond, num_layers=args.layers)
     nccl_id = None
-    if world > 1:
+    if world > 1 and not GLOO_TEST:
         obj = [lp.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     eng = lp.LpEngine(DIMS, PATCH, 4, K, R_OVERLAP, T_SCHED, ETA, W_CFG, cond, denoiser="dit", dit=dit, world=world,
                       rank=rank, nccl_id=nccl_id, group_size=M)
+    exchange = "nccl" if world > 1 else "none"
+    if world > 1 and M == 1 and args.exchange == "peer":
+        # K9 over NVLink peer memory (CUDA IPC); every rank must map every peer, else all stay on NCCL
+        handles = [None] * world
+        dist.all_gather_object(handles, eng.ipc_handle())
+        ok = 1
+        try:
+            eng.ipc_attach(handles)
+        except Exception as ex:  # noqa: BLE001
+            print(f"rank {rank}: peer attach failed ({ex}); exchanging through NCCL", file=sys.stderr)
+            ok = 0
+        t = torch.tensor([ok], dtype=torch.int32, device="cpu" if GLOO_TEST else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if int(t.item()) == 1:
+            exchange = "peer"
+        elif ok:
+            eng.ipc_detach()
     z0 = torch.from_numpy(z_host_np.astype("float32")).pin_memory()
     eng.z.data.copy_(z0)
     stream = torch.cuda.current_stream()
@@ -255,7 +278,7 @@ def run_ours(args, rank, world, local_rank):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if GLOO_TEST else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -300,6 +323,8 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
     assert torch.isfinite(zout).all(), "non-finite latent"
+    if lp.device_flags(reset=True) & 4:
+        raise SystemExit(f"rank {rank}: peer exchange watchdog fired (a peer's epoch flag never arrived)")
 
     # ---- per-kernel roofline pass: one rotation cycle (T, H, W) with the shard streams
     # serialised, so each kernel's CUDA-event duration is its own (in the timed region two
@@ -390,6 +415,7 @@ def run_ours(args, rank, world, local_rank):
         "hbm_kernels": hbm,
         "allgather": ag,
         "clocks": clk.summary(),
+        "exchange": exchange,
         "comm": {"nccl_bytes_per_step_measured_all_ranks": per_step_nccl,
                  "allgather_bytes_per_video": ag_video, "reference_ledger_bytes_per_video": led,
                  "reference_nmp_bytes_per_video": nmp, "wire": "f32 eps shards (ledger counts the 2-B preset width)"},
@@ -426,6 +452,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workers", type=int, default=0, help="LP workers K (default max(4, N))")
     ap.add_argument("--layers", type=int, default=30)
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: eps exchange over NVLink peer memory fused into the DiT epilogue (default), or NCCL")
     ap.add_argument("--hybrid", type=int, default=1,
                     help="M > 1: hybrid LP x model parallelism, N/M LP groups of M pipeline stages (K = N/M)")
     ap.add_argument("--overlap", type=float, default=None,
@@ -438,7 +466,7 @@ def main():
         R_OVERLAP = args.overlap
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    local_rank = 0 if GLOO_TEST else int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
@@ -447,7 +475,10 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if GLOO_TEST:  # validation of the multi-rank bench on ONE GPU: gloo plumbing, peer exchange
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

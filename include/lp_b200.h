@@ -295,6 +295,9 @@ int lp_dit_forward_layers(lp_dit* dit, int32_t slot, const void* sub, const int6
 /* The slot's activation (fp32 residual stream [2 * tokens, dim]) for a shard of `shape`:
  * what one pipeline stage hands the next (bytes = 2 * tokens * dim * 4). */
 int lp_dit_activation(lp_dit* dit, int32_t slot, const int64_t shape[4], void** x_dptr, int64_t* bytes);
+/* K8+K9 fusion for the engine's peer exchange: while n > 0 the CFG-combine epilogue stores
+ * every ε̂ element also at eps_out + byte_deltas[j] (peer gather buffers mapped by CUDA IPC). */
+int lp_dit_set_mirrors(lp_dit* dit, int32_t n, const int64_t* byte_deltas);
 /* cfg_predict with the DiT: CFG batch 2 (uncond = null text, cond = synthetic
  * text), one forward, combine uncond + w*(cond-uncond), quantize to dtype. */
 int lp_dit_cfg_predict(lp_dit* dit, const void* sub, const int64_t shape[4], int dtype_bytes, int timestep,
@@ -379,6 +382,17 @@ int lp_engine_gather_buffer(const lp_engine* e, int32_t step, void** buffer, int
  * activations move by ncclSend/Recv; phase 2 broadcasts each group's slot from its last
  * stage. */
 int lp_engine_stage(lp_engine* e, int32_t step, int32_t idx, void* stream);
+/* K9 over NVLink peer memory instead of NCCL (plain LP engines created without an NCCL id):
+ * every rank exports its exchange arena (double-buffered gather buffer + flag words) with
+ * lp_engine_ipc_handle, the caller all-gathers the 64-byte handles, and lp_engine_ipc_attach
+ * maps the peers' arenas (CUDA IPC); with an NCCL communicator too, the peer path takes
+ * precedence for the ε̂ exchange.  lp_engine_run then pushes this rank's ε̂ slot into every
+ * peer with remote stores and a system-scope release flag per step, and K10 starts once every
+ * peer's flag for the step has arrived. */
+int lp_engine_ipc_handle(lp_engine* e, uint8_t handle_out[64]);
+int lp_engine_ipc_attach(lp_engine* e, const uint8_t* handles /* world x 64 bytes, by rank */);
+/* Unmaps the peers and returns the exchange to NCCL (or to the caller). */
+int lp_engine_ipc_detach(lp_engine* e);
 int lp_engine_stage_activation(lp_engine* e, int32_t step, int32_t idx, void** x_dptr, int64_t* bytes);
 int lp_engine_owned(const lp_engine* e, int32_t step, int32_t* n_owned);
 /* Group decomposition of this rank and the activation bytes it handed to the next stage. */

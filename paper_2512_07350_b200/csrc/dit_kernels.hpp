@@ -37,7 +37,13 @@ void rope_table(float2* tab, int nf, int nh, int nw, cudaStream_t st);
 bool rmsnorm_rope_tab(__nv_bfloat16* buf, int64_t rows, int64_t ld, int64_t col0, int d, int nsec, const float* g0,
                       const float* g1, float eps, const float2* tab, int64_t rows_per_batch, int nf, int nh, int nw,
                       cudaStream_t st);
+// Peer copies of the ε̂ written by unpatchify_cfg: element i is also stored at
+// (char*)(eps + i) + delta[j] (an IPC-mapped peer gather buffer), j < n.
+struct EpsMirrors {
+    int n = 0;
+    int64_t delta[16] = {};
+};
 void unpatchify_cfg(const float* head, int dtype, const int shape[4], const int patch[3], double w, void* eps,
-                    cudaStream_t st);
+                    cudaStream_t st, const EpsMirrors& mr = EpsMirrors());
 
 }  // namespace lpb200

@@ -52,6 +52,14 @@ struct lp_engine {
     // `stage` of LP group `group`, running DiT blocks [layer0, layer1)
     int M = 1, groups = 1, group = 0, stage = 0, layer0 = 0, layer1 = 0;
     uint64_t intra_bytes = 0;  // activation bytes this rank sent to the next stage
+    // exchange over CUDA-IPC peer memory (lp_engine_ipc_attach): arena = 2 gather buffers
+    // (epoch parity) + per-rank flag words + the push kernel's arrival counter
+    uint8_t* arena = nullptr;
+    size_t gather_bytes = 0, flags_off = 0;
+    bool peer = false;
+    uint8_t* peer_arena[kMaxPeers + 1] = {};
+    unsigned long long epoch = 0;
+    uint64_t peer_bytes = 0;
     // DiT engines replay each axis's step as a CUDA graph (captured the second time the
     // axis comes up, so every kernel's one-time setup has run eagerly first)
     cudaGraphExec_t graph[3] = {};
@@ -124,8 +132,12 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
             }
             const size_t E = static_cast<size_t>(c->dtype_bytes);
             LP_CUDA(cudaMalloc(&e->z, static_cast<size_t>(e->shape.volume()) * E));
-            LP_CUDA(cudaMalloc(&e->gather, static_cast<size_t>(max_slot) * e->groups * E));
-            LP_CUDA(cudaMemset(e->gather, 0, static_cast<size_t>(max_slot) * e->groups * E));
+            e->gather_bytes = (static_cast<size_t>(max_slot) * e->groups * E + 255) / 256 * 256;
+            e->flags_off = 2 * e->gather_bytes;
+            const size_t arena = e->flags_off + (static_cast<size_t>(c->world) * 8 + 8 + 255) / 256 * 256;
+            LP_CUDA(cudaMalloc(&e->arena, arena));
+            LP_CUDA(cudaMemset(e->arena, 0, arena));
+            e->gather = e->arena;
             size_t max_owned = 1;
             for (int a = 0; a < 3; ++a) max_owned = std::max(max_owned, e->layout[a].owned.size());
             const int want_slots = std::max(1, std::min(4, tune_get("engine_slots", 2)));
@@ -182,7 +194,9 @@ int lp_engine_destroy(lp_engine* e) {
     if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
     if (e->comm) ncclCommDestroy(e->comm);
     cudaFree(e->z);
-    cudaFree(e->gather);
+    for (auto* p : e->peer_arena)
+        if (p) cudaIpcCloseMemHandle(p);
+    cudaFree(e->arena);
     cudaFree(e->sub);
     for (int s = 0; s < 4; ++s) {
         if (e->slot_stream[s]) cudaStreamDestroy(e->slot_stream[s]);
@@ -334,7 +348,7 @@ void step_reconstruct(lp_engine* e, int i, cudaStream_t st) {
 void account_step(lp_engine* e, int i) {
     const lp_engine_config& c = e->cfg;
     const int a = step_axis(e, i);
-    if (e->comm) {
+    if (e->comm && !e->peer) {
         const int foreign = e->M == 1 ? c.world - 1 : e->groups - (e->stage == e->M - 1 ? 1 : 0);
         e->nccl_bytes += static_cast<size_t>(e->layout[a].slot_elems) * c.dtype_bytes * foreign;
     }
@@ -343,9 +357,53 @@ void account_step(lp_engine* e, int i) {
     e->ledger_bytes += 4ull * sum * static_cast<uint64_t>(c.wire_bytes);
 }
 
+// K9 over peer memory: push this rank's slot into every peer's buffer of the current parity,
+// publish the epoch, wait for every peer's epoch (engine exchange mode "peer").
+void step_exchange_peer(lp_engine* e, int i, cudaStream_t st, bool fused) {
+    const lp_engine_config& c = e->cfg;
+    const ShardLayout& L = e->layout[step_axis(e, i)];
+    const size_t slot = static_cast<size_t>(L.slot_elems) * c.dtype_bytes;
+    const size_t parity = static_cast<size_t>(e->epoch & 1) * e->gather_bytes;
+    PeerPush pp{};
+    pp.local = static_cast<const uint8_t*>(e->gather);
+    for (int j = 0; j < c.world; ++j) {
+        if (j == c.rank) continue;
+        pp.peer[pp.npeers] = e->peer_arena[j] + parity;
+        pp.peer_flag[pp.npeers] = reinterpret_cast<unsigned long long*>(e->peer_arena[j] + e->flags_off) + c.rank;
+        ++pp.npeers;
+    }
+    pp.off = slot * static_cast<size_t>(c.rank);
+    pp.bytes = fused ? 0 : slot;  // fused: the slot already went out with the DiT epilogue; signal only
+    pp.epoch = e->epoch;
+    prof_begin(KC_ALLGATHER, st);
+    peer_push(pp, reinterpret_cast<unsigned*>(e->arena + e->flags_off + static_cast<size_t>(c.world) * 8), st);
+    peer_wait(reinterpret_cast<const unsigned long long*>(e->arena + e->flags_off), c.world, c.rank, e->epoch, st);
+    prof_end(KC_ALLGATHER, st, 0.0, static_cast<double>(slot) * (c.world - 1));
+    e->peer_bytes += static_cast<uint64_t>(slot) * (c.world - 1);
+}
+
 void run_step_eager(lp_engine* e, int i, cudaStream_t st) {
-    step_compute(e, i, st);
-    if (e->comm) step_exchange(e, i, st);
+    if (e->peer) {  // double-buffered gather by epoch parity
+        ++e->epoch;
+        e->gather = e->arena + static_cast<size_t>(e->epoch & 1) * e->gather_bytes;
+    }
+    const bool fused = e->peer && e->cfg.dit && tune_get("peer_fused", 1);
+    if (fused) {  // K8+K9: the DiT epilogue stores ε̂ into every peer's buffer as it computes it
+        std::vector<int64_t> deltas;
+        for (int j = 0; j < e->cfg.world; ++j)
+            if (j != e->cfg.rank) deltas.push_back(static_cast<int64_t>(e->peer_arena[j] - e->arena));
+        const int rc = lp_dit_set_mirrors(e->cfg.dit, static_cast<int>(deltas.size()), deltas.data());
+        if (rc) fail(rc, lp_last_error());
+    }
+    try {
+        step_compute(e, i, st);
+    } catch (...) {
+        if (fused) lp_dit_set_mirrors(e->cfg.dit, 0, nullptr);
+        throw;
+    }
+    if (fused) lp_dit_set_mirrors(e->cfg.dit, 0, nullptr);
+    if (e->peer) step_exchange_peer(e, i, st, fused);
+    else if (e->comm) step_exchange(e, i, st);
     step_reconstruct(e, i, st);
 }
 
@@ -397,15 +455,16 @@ extern "C" {
 int lp_engine_run(lp_engine* e, int32_t first, int32_t count, void* stream) {
     return guard([&] {
         cudaStream_t st = as_stream(stream);
-        if (e->cfg.world > 1 && !e->comm)
+        if (e->cfg.world > 1 && !e->comm && !e->peer)
             fail(LP_ERR_INVALID_ARGUMENT,
-                 "world > 1 without an NCCL id: drive the steps with lp_engine_step_phase and an external exchange");
+                 "world > 1 without an NCCL id or peer attach: drive the steps with lp_engine_step_phase and an "
+                 "external exchange");
         const uint64_t l0 = launch_count();
         // graphs: DiT engines, on a stream that can be captured, unless per-launch profiling
         // or the serialised debug mode is on (both need the eager launches)
         // (multi-rank engines stay eager: their step holds an ncclAllGather, and a capture
         // failure there would cost a scaling run for no device-time gain — DESIGN.md §6)
-        const bool graphs = e->cfg.dit != nullptr && e->comm == nullptr && tune_get("engine_graph", 1) &&
+        const bool graphs = e->cfg.dit != nullptr && e->comm == nullptr && !e->peer && tune_get("engine_graph", 1) &&
                             !prof_enabled() && !tune_get("engine_serial", 0);
         for (int i = first; i < first + count; ++i) {
             if (graphs) run_step_graph(e, i, st);
@@ -481,8 +540,46 @@ int lp_engine_gather_buffer(const lp_engine* e, int32_t step, void** buffer, int
     });
 }
 
+int lp_engine_ipc_handle(lp_engine* e, uint8_t handle_out[64]) {
+    return guard([&] {
+        cudaIpcMemHandle_t h;
+        LP_CUDA(cudaIpcGetMemHandle(&h, e->arena));
+        static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+        std::memcpy(handle_out, &h, 64);
+    });
+}
+
+int lp_engine_ipc_attach(lp_engine* e, const uint8_t* handles) {
+    return guard([&] {
+        const lp_engine_config& c = e->cfg;
+        if (e->M > 1) fail(LP_ERR_INVALID_GROUPING, "peer exchange is for plain LP engines (group_size 1)");
+        if (c.world < 2 || c.world > kMaxPeers + 1) fail(LP_ERR_INVALID_ARGUMENT, "peer exchange needs 2..17 ranks");
+        for (int j = 0; j < c.world; ++j) {
+            if (j == c.rank) continue;
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, handles + 64 * static_cast<size_t>(j), 64);
+            void* p = nullptr;
+            LP_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            e->peer_arena[j] = static_cast<uint8_t*>(p);
+        }
+        e->peer = true;  // takes precedence over an NCCL communicator for the ε̂ exchange
+    });
+}
+
+int lp_engine_ipc_detach(lp_engine* e) {
+    return guard([&] {
+        for (auto*& p : e->peer_arena)
+            if (p) {
+                LP_CUDA(cudaIpcCloseMemHandle(p));
+                p = nullptr;
+            }
+        e->peer = false;
+        e->gather = e->arena;
+    });
+}
+
 int lp_engine_comm(const lp_engine* e, uint64_t* nccl_bytes, uint64_t* ledger_bytes) {
-    *nccl_bytes = e->nccl_bytes;
+    *nccl_bytes = e->nccl_bytes + e->peer_bytes;
     *ledger_bytes = e->ledger_bytes;
     return LP_OK;
 }

@@ -284,6 +284,75 @@ void slice_to(const void* z, const Shape4& s, int axis, i64 begin, i64 end, int 
 }
 
 // ---------------------------------------------------------------------------
+// K9 over peer memory (the engine's NVLink exchange; CUDA-IPC-mapped gather buffers).
+// k_peer_push: rank r copies its own slot [off, off+bytes) of the local gather buffer to the
+// same offset of every peer's buffer with 16-B remote stores, then the last block to finish
+// (a grid-wide arrival counter) publishes `epoch` into every peer's flag word for rank r
+// with a system-scope release.  k_peer_wait: spins (system-scope acquire) until every peer's
+// flag for this rank's buffer reaches `epoch`; a 10 s clock64 watchdog raises
+// LP_FLAG_PEER_TIMEOUT instead of hanging.  The gather buffer is double-buffered by epoch
+// parity, so a push for step i+1 never lands in a buffer a peer's K10 of step i still reads.
+// ---------------------------------------------------------------------------
+constexpr unsigned LP_FLAG_PEER_TIMEOUT = 4u;
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(256) k_peer_push(const __grid_constant__ PeerPush pp, unsigned* counter) {
+    const uint64_t nvec = pp.bytes / 16;
+    const uint4* src = reinterpret_cast<const uint4*>(pp.local + pp.off);
+    for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < nvec;
+         v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint4 x = __ldg(src + v);
+        for (int j = 0; j < pp.npeers; ++j) reinterpret_cast<uint4*>(pp.peer[j] + pp.off)[v] = x;
+    }
+    // tail bytes (slot sizes are element multiples, not always 16-B multiples)
+    if (blockIdx.x == 0)
+        for (uint64_t b = nvec * 16 + threadIdx.x; b < pp.bytes; b += blockDim.x)
+            for (int j = 0; j < pp.npeers; ++j) pp.peer[j][pp.off + b] = pp.local[pp.off + b];
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned done = atomicAdd(counter, 1u);
+        if (done == gridDim.x - 1) {
+            __threadfence_system();
+            for (int j = 0; j < pp.npeers; ++j) st_release_sys(pp.peer_flag[j], pp.epoch);
+            *counter = 0;
+        }
+    }
+}
+
+__global__ void k_peer_wait(const unsigned long long* flags, int world, int rank, unsigned long long epoch) {
+    const int j = threadIdx.x;
+    if (j >= world || j == rank) return;
+    const long long t0 = clock64();
+    while (ld_acquire_sys(flags + j) < epoch) {
+        if (clock64() - t0 > (1ll << 35)) {  // ~10-20 s: a dead peer, not a slow one
+            raise_flag(LP_FLAG_PEER_TIMEOUT);
+            return;
+        }
+        __nanosleep(200);
+    }
+}
+
+void peer_push(const PeerPush& pp, unsigned* counter, cudaStream_t st) {
+    const int g = grid_for(static_cast<int64_t>(pp.bytes / 16) + 1, 256, 4);
+    k_peer_push<<<g, 256, 0, st>>>(pp, counter);
+    LP_LAUNCH_CHECK();
+}
+
+void peer_wait(const unsigned long long* flags, int world, int rank, unsigned long long epoch, cudaStream_t st) {
+    k_peer_wait<<<1, 32 * ((world + 31) / 32), 0, st>>>(flags, world, rank, epoch);
+    LP_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
 // K11: toy denoisers (src/denoise.cpp:56-142), fp64 in the reference order.
 // MODE 0: plain predict (affine a0) -> out.
 // MODE 1: fused cfg_predict: u = q(m + a0), c = q(m + a1), out = q(u + w(c-u)).

@@ -38,4 +38,17 @@ void slice_to(const void* z, const Shape4& s, int axis, i64 begin, i64 end, int 
 void gather_entries(const void* z, const Shape4& s, const lp_plan& plan, const int* ks, int count, int E, void* dst,
                     cudaStream_t st);
 
+// K9 over CUDA-IPC peer memory (engine exchange mode "peer").
+constexpr int kMaxPeers = 16;
+struct PeerPush {
+    const uint8_t* local;                      // this rank's gather buffer (current parity)
+    uint8_t* peer[kMaxPeers];                  // the peers' gather buffers (same parity)
+    unsigned long long* peer_flag[kMaxPeers];  // &flags_of_peer[rank]
+    uint64_t off, bytes;                       // this rank's slot
+    unsigned long long epoch;
+    int npeers;
+};
+void peer_push(const PeerPush& pp, unsigned* counter, cudaStream_t st);
+void peer_wait(const unsigned long long* flags, int world, int rank, unsigned long long epoch, cudaStream_t st);
+
 }  // namespace lpb200

@@ -534,6 +534,20 @@ class LpEngine:
         dt = getattr(torch, _TORCH_DT[self.dtype_bytes])
         return _wrap_device(ptr.value, self.groups * slot.value, dt), slot.value
 
+    # --- K9 over NVLink peer memory (CUDA IPC) instead of NCCL ---
+    def ipc_handle(self) -> bytes:
+        h = (C.c_uint8 * 64)()
+        check(lib().lp_engine_ipc_handle(self.handle, h))
+        return bytes(h)
+
+    def ipc_attach(self, handles):
+        """handles: the world ranks' ipc_handle() bytes, by rank."""
+        buf = (C.c_uint8 * (64 * len(handles)))(*b"".join(handles))
+        check(lib().lp_engine_ipc_attach(self.handle, buf))
+
+    def ipc_detach(self):
+        check(lib().lp_engine_ipc_detach(self.handle))
+
     # --- hybrid LP x model-parallel groups (group_size > 1), SURVEY.md §8 f2 ---
     def owned(self, step):
         n = C.c_int32()

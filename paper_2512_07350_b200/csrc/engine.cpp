@@ -39,11 +39,10 @@ struct lp_engine {
     ReconParams recon[3];
     void* z = nullptr;
     void* gather = nullptr;
-    void* sub = nullptr;  // [nslots][max_entry]
+    void* sub = nullptr;  // K1 output: the step's owned entries, packed in owned order
     double* ws = nullptr;
     // owned entries' DiT forwards overlap on nslots streams (world == 1: K shards on one GPU)
     int nslots = 1;
-    size_t sub_stride = 0;
     cudaStream_t slot_stream[4] = {};
     cudaEvent_t ev_fork = nullptr, ev_join[4] = {};
     ncclComm_t comm = nullptr;
@@ -120,7 +119,7 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
             e->cond_mean = acc / static_cast<double>(n_cond);
         }
         try {
-            i64 max_slot = 0, max_entry = 0;
+            i64 max_slot = 0;
             for (int a = 0; a < 3; ++a) {
                 // step index a+1 has axis a; step_index is cosmetic in the plan
                 e->plans[a] = build_plan_for_shape(e->shape, c->patch, a + 1, c->workers, c->overlap_ratio);
@@ -128,7 +127,6 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
                 e->elems[a] = entry_elems(e->plans[a], e->shape);
                 e->recon[a] = make_recon_params(e->plans[a], e->shape, e->layout[a].base, c->eta);
                 max_slot = std::max(max_slot, e->layout[a].slot_elems);
-                for (i64 n : e->elems[a]) max_entry = std::max(max_entry, n);
             }
             const size_t E = static_cast<size_t>(c->dtype_bytes);
             LP_CUDA(cudaMalloc(&e->z, static_cast<size_t>(e->shape.volume()) * E));
@@ -149,7 +147,6 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
                 for (int k : e->layout[a].owned) tot += static_cast<size_t>(e->elems[a][k]);
                 max_owned_elems = std::max(max_owned_elems, tot);
             }
-            (void)max_entry;
             LP_CUDA(cudaMalloc(&e->sub, max_owned_elems * E));
             LP_CUDA(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
             for (int s = 0; s < e->nslots; ++s) {

@@ -320,6 +320,11 @@ int lp_dit_debug_tensor(const lp_dit* dit, const char* name, void** dptr, int64_
 /* D[M,N] (bf16, row-major) = A[M,K] (bf16, row-major) · B[N,K]^T (bf16) + bias[N] (f32 or NULL). */
 int lp_gemm_bf16(const void* A, const void* B, const void* bias, void* D, int64_t M, int64_t N, int64_t K,
                  void* stream);
+/* The same GEMM with the DiT's fused epilogues (kernel tests / benches): mode 0 = bf16
+ * D = AB^T + bias; 1 = bf16 GELU(tanh); 2 = fp32 residual D += gate ⊙ (AB^T + bias)
+ * (gate may be NULL = 1); 3 = fp32 D = AB^T + bias.  D row stride = N. */
+int lp_gemm_bf16_epi(const void* A, const void* B, const void* bias, const float* gate, void* D, int64_t M, int64_t N,
+                     int64_t K, int32_t mode, void* stream);
 /* Flash attention forward (tcgen05): q,k,v,o bf16 [B, S, H, 128] row-major. */
 int lp_attention_bf16(const void* q, const void* k, const void* v, void* o, int64_t batch, int64_t seq_q,
                       int64_t seq_kv, int64_t heads, double scale, void* stream);

@@ -129,6 +129,7 @@ _SIGS = {
     "lp_engine_step_phase": (_i, [_vp, _i32, _i32, _vp]),
     "lp_engine_gather_buffer": (_i, [_vp, _i32, C.POINTER(_vp), C.POINTER(_i64)]),
     "lp_engine_stage": (_i, [_vp, _i32, _i32, _vp]),
+    "lp_gemm_bf16_epi": (_i, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i32, _vp]),
     "lp_engine_ipc_handle": (_i, [_vp, C.POINTER(C.c_uint8)]),
     "lp_engine_ipc_attach": (_i, [_vp, C.POINTER(C.c_uint8)]),
     "lp_engine_ipc_detach": (_i, [_vp]),

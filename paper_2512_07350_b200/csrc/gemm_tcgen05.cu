@@ -64,6 +64,22 @@ CUtensorMap make_tmap_2d_bf16(const void* base, uint64_t inner, uint64_t outer, 
     return m;
 }
 
+// Output / residual map of the TMA-staged epilogue: [rows, cols] of fp32 or bf16 with a
+// 32 x 32 box; the box's inner extent is 128 B (fp32, 128B swizzle) or 64 B (bf16, 64B swizzle).
+static CUtensorMap make_tmap_epi(void* base, bool f32, uint64_t cols, uint64_t rows, uint64_t ld_elems) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {ld_elems * (f32 ? 4 : 2)};
+    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base,
+                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(LP_ERR_CUDA, "cuTensorMapEncodeTiled(epilogue) failed: " + std::to_string(r));
+    return m;
+}
+
 CUtensorMap make_tmap_3d_bf16(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
                               uint32_t b0, uint32_t b1, uint32_t b2) {
     CUtensorMap m;
@@ -243,6 +259,81 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// TMA-staged epilogue (CTA-pair kernel).  Each epilogue warp owns 32 accumulator rows; per
+// 32-column chunk it writes its 32 x 32 block into a swizzled shared-memory box and ONE
+// lane issues a TMA tensor store of the box — full 128-B lines, no per-row LSU traffic.  The
+// fp32 residual epilogue first TMA-loads the x box into the same buffer, one chunk AHEAD
+// (double-buffered per warp, the chunk sequence runs across tiles), so the load overlaps
+// the previous chunk.  Swizzle (matches the tensor maps): fp32 rows are 128 B, 16-B unit
+// j of row r sits at unit j ^ (r & 7); bf16 rows are 64 B, unit j at j ^ ((r >> 1) & 3) —
+// a lane-per-row access then spreads over all banks (4 wavefronts per 512 B).
+// ---------------------------------------------------------------------------
+constexpr int kEpiBox = 4096;  // one 32 x 32 fp32 box (bf16 uses the first 2 KB)
+#ifndef LP_EPI_LSU
+constexpr bool kEpiTma = true;
+#else
+constexpr bool kEpiTma = false;  // A/B build: thread-per-row LSU stores
+#endif
+
+__device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(smem_u32(smem)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_cta(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(smem)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+template <int MODE>
+__device__ __forceinline__ void epi_chunk_smem(const GemmEpilogue& ep, int col0, const uint32_t (&r)[32], uint8_t* box) {
+    const uint32_t lane = lane_id();
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+        const float4 b = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[j] = __uint_as_float(r[j]) + b.x;
+        v[j + 1] = __uint_as_float(r[j + 1]) + b.y;
+        v[j + 2] = __uint_as_float(r[j + 2]) + b.z;
+        v[j + 3] = __uint_as_float(r[j + 3]) + b.w;
+    }
+    if (MODE == EPI_BF16 || MODE == EPI_BF16_GELU) {
+        uint8_t* row = box + lane * 64;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float a[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] = MODE == EPI_BF16_GELU ? gelu_tanh(v[8 * j + u]) : v[8 * j + u];
+            *reinterpret_cast<uint4*>(row + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
+        }
+    } else {
+        uint8_t* row = box + lane * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float4* p = reinterpret_cast<float4*>(row + ((j ^ (lane & 7)) << 4));
+            float4 x;
+            if (MODE == EPI_F32_RESID) {
+                x = *p;
+                const float4 g = ep.gate ? __ldg(reinterpret_cast<const float4*>(ep.gate + col0 + 4 * j))
+                                         : make_float4(1.f, 1.f, 1.f, 1.f);
+                x.x += v[4 * j] * g.x;
+                x.y += v[4 * j + 1] * g.y;
+                x.z += v[4 * j + 2] * g.z;
+                x.w += v[4 * j + 3] * g.w;
+            } else {
+                x = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
+            *p = x;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // CTA-pair variant (cta_group::2): a 2-CTA cluster computes a 256 x BN tile with
 // one UMMA_M = 256 instruction stream issued by the leader CTA.  Each CTA TMA-loads
 // its own 128 rows of A and BN/2 rows of B (half the B bytes per SM of the 1-CTA
@@ -253,24 +344,26 @@ template <int BN>
 constexpr int gemm2_stages() { return BN == 256 ? 6 : 8; }
 template <int BN>
 constexpr int gemm2_smem_bytes() {
-    return gemm2_stages<BN>() * (kBM * kBK * 2 + (BN / 2) * kBK * 2) + 1024 + 256;
+    return gemm2_stages<BN>() * (kBM * kBK * 2 + (BN / 2) * kBK * 2) + 1024 + 256 + (kEpiTma ? 8 * kEpiBox : 0);
 }
 
 template <int BN, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
-    k_gemm2(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, GemmEpilogue ep, int M,
-            int N, int K) {
+    k_gemm2(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
+            const __grid_constant__ CUtensorMap tmo, GemmEpilogue ep, int M, int N, int K) {
     constexpr int S = gemm2_stages<BN>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int A_BYTES = kBM * kBK * 2, B_BYTES = (BN / 2) * kBK * 2;
     uint8_t* sA = smem;
     uint8_t* sB = smem + S * A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * B_BYTES);
+    uint8_t* sE = sB + S * B_BYTES;  // [4 epilogue warps][2][kEpiBox] (1024-aligned)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sE + (kEpiTma ? 8 * kEpiBox : 0));
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* ebar = tempty + 2;  // [4 warps][2] residual-box loads
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 8);
 
     const uint32_t warp = warp_id(), lane = lane_id();
     const uint32_t rank = cluster_ctarank();
@@ -289,6 +382,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 256);  // both CTAs' epilogue threads arrive on the leader's
         }
+        for (int b = 0; b < 8; ++b) mbar_init(&ebar[b], 1);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc_2sm(tmem_slot, 2 * BN);
@@ -348,6 +442,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 __syncwarp();
             }
         }
+    } else if (kEpiTma) {
+        const uint32_t q = warp & 3;
+        uint8_t* boxes = sE + q * 2 * kEpiBox;
+        uint64_t* wbar = ebar + q * 2;
+        constexpr int NCH = BN / 32;
+        constexpr bool RESID = MODE == EPI_F32_RESID;
+        uint32_t lph[2] = {0, 0};
+        // chunk sequence u = (tile it, chunk c) in order; the residual box of u+1 is loaded
+        // while u is combined.  Buffer of u = u & 1.
+        auto issue_load = [&](int t, int c, int b) {
+            if (lane == 0) {
+                bulk_wait_read<0>();  // the store that last read buffer b (chunk u-1) is done
+                mbar_arrive_expect_tx(&wbar[b], kEpiBox);
+                tma_load_2d_cta(&tmo, &wbar[b], boxes + b * kEpiBox, (t % num_n) * BN + c * 32,
+                                (t / num_n) * 2 * kBM + rank * kBM + q * 32);
+            }
+        };
+        int u = 0;
+        if (RESID && cluster < tiles) issue_load(cluster, 0, 0);
+        int it = 0;
+        for (int t = cluster; t < tiles; t += nclusters, ++it) {
+            const int mb = t / num_n, nb = t % num_n;
+            const int acc = it & 1;
+            const uint32_t aph = (it >> 1) & 1;
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            const int row0 = mb * 2 * kBM + rank * kBM + q * 32;
+            const uint32_t taddr = tmem + ((q * 32) << 16) + acc * BN;
+#pragma unroll 1
+            for (int c = 0; c < NCH; ++c, ++u) {
+                const int b = u & 1;
+                uint32_t r[32];
+                tmem_ld32(taddr + c * 32, r);
+                if (RESID) {
+                    // next chunk's residual box (may belong to the next tile)
+                    if (c + 1 < NCH) issue_load(t, c + 1, b ^ 1);
+                    else if (t + nclusters < tiles) issue_load(t + nclusters, 0, b ^ 1);
+                    mbar_wait(&wbar[b], lph[b]);
+                    lph[b] ^= 1;
+                } else if (lane == 0) {
+                    bulk_wait_read<1>();  // the store issued from this buffer two chunks ago has read it
+                }
+                __syncwarp();
+                tmem_ld_wait();
+                epi_chunk_smem<MODE>(ep, nb * BN + c * 32, r, boxes + b * kEpiBox);
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tmo, boxes + b * kEpiBox, nb * BN + c * 32, row0);
+                    bulk_commit();
+                }
+            }
+            tc_fence_before();
+            mbar_arrive_cluster(&tempty[acc], 0);
+        }
+        if (lane == 0) bulk_wait_all();
+        __syncwarp();
     } else {
         const uint32_t q = warp & 3;
         int it = 0;
@@ -406,6 +557,8 @@ static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Gemm
 template <int BN, int MODE>
 static void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmEpilogue& ep, int M, int N, int K,
                          cudaStream_t st) {
+    const CUtensorMap to = make_tmap_epi(ep.out, MODE >= EPI_F32_RESID, static_cast<uint64_t>(N), static_cast<uint64_t>(M),
+                                         static_cast<uint64_t>(ep.ldo));
     constexpr int smem = gemm2_smem_bytes<BN>();
     static bool attr = false;
     if (!attr) {
@@ -414,7 +567,7 @@ static void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const Gem
     }
     const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * (N / BN);
     const int clusters = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-    k_gemm2<BN, MODE><<<2 * clusters, kGemmThreads, smem, st>>>(ta, tb, ep, M, N, K);
+    k_gemm2<BN, MODE><<<2 * clusters, kGemmThreads, smem, st>>>(ta, tb, to, ep, M, N, K);
     LP_LAUNCH_CHECK();
 }
 
@@ -467,6 +620,20 @@ void gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int M, in
 }  // namespace lpb200
 
 using namespace lpb200;
+
+extern "C" int lp_gemm_bf16_epi(const void* A, const void* B, const void* bias, const float* gate, void* D,
+                                int64_t M, int64_t N, int64_t K, int32_t mode, void* stream) {
+    return guard([&] {
+        if (mode < EPI_BF16 || mode > EPI_F32) fail(LP_ERR_INVALID_ARGUMENT, "epilogue mode 0..3");
+        GemmEpilogue ep{};
+        ep.bias = static_cast<const float*>(bias);
+        ep.out = D;
+        ep.ldo = N;
+        ep.gate = gate;
+        gemm_bf16(A, K, B, K, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), ep, mode,
+                  as_stream(stream));
+    });
+}
 
 extern "C" int lp_gemm_bf16(const void* A, const void* B, const void* bias, void* D, int64_t M, int64_t N, int64_t K,
                             void* stream) {

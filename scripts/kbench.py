@@ -47,6 +47,23 @@ for (M, N, K, name) in ([] if "attn" in sys.argv else GEMMS):
                            "cublas_ms": tc, "cublas_tflops": 2 * M * N * K / tc / 1e9}
     print(json.dumps({f"gemm_{name}": out[f"gemm_{name}"]}), flush=True)
     del A, B, D
+# the DiT's fused epilogues at the shard size: GELU (ffn1) and the fp32 gated residual (o / co / ffn2)
+for (M, N, K, mode, name) in ([] if "attn" in sys.argv or "gemm" in sys.argv and "epi" not in sys.argv else
+                              [(R, 8960, 1536, 1, "ffn1_gelu"), (R, 1536, 1536, 2, "o_resid"),
+                               (R, 1536, 8960, 2, "ffn2_resid")]):
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = torch.randn(N, K, device="cuda").bfloat16()
+    bias = torch.randn(N, device="cuda")
+    gate = torch.randn(N, device="cuda")
+    D = torch.zeros(M, N, device="cuda", dtype=torch.float32 if mode >= 2 else torch.bfloat16)
+    f = lambda: _lib.check(L.lp_gemm_bf16_epi(C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()),  # noqa: E731
+                                              C.c_void_p(bias.data_ptr()), C.c_void_p(gate.data_ptr()),
+                                              C.c_void_p(D.data_ptr()), M, N, K, mode, st()))
+    ms = timeit(f)
+    out[f"gemm_{name}"] = {"M": M, "N": N, "K": K, "mode": mode, "ms": ms, "tflops": 2 * M * N * K / ms / 1e9,
+                           "epilogue_GBps": (M * N * (8 if mode == 2 else 2)) / ms / 1e6}
+    print(json.dumps({f"gemm_{name}": out[f"gemm_{name}"]}), flush=True)
+    del A, B, D
 for (S, name) in ([] if "gemm" in sys.argv else [(32760, "self_k1"), (18720, "self_k4max"), (14040, "self_k4min")]):
     q = torch.randn(2, S, 12, 128, device="cuda").bfloat16()
     k = torch.randn(2, S, 12, 128, device="cuda").bfloat16()

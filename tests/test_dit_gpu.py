@@ -40,6 +40,26 @@ def test_gemm_matches_torch(cuda, M, N, K):
     assert err <= 2e-2 * ref.abs().max().item() + 1e-2, err
 
 
+@pytest.mark.parametrize("mode", [0, 1, 2, 3], ids=["bf16", "bf16-gelu", "f32-resid", "f32"])
+@pytest.mark.parametrize("M,N,K", [(300, 1536, 1536), (1000, 8960, 512), (4097, 1536, 8960), (257, 256, 128)])
+def test_gemm_fused_epilogues_match_torch(cuda, mode, M, N, K):
+    """The DiT's fused epilogues (lp_gemm_bf16_epi): bias, tanh-GELU, fp32 gated residual."""
+    g = torch.Generator(device="cuda").manual_seed(M + 3 * N + 7 * K + mode)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g)
+    gate = torch.randn(N, device="cuda", generator=g)
+    x0 = torch.randn(M, N, device="cuda", generator=g)
+    D = x0.clone() if mode == 2 else torch.empty(M, N, device="cuda", dtype=torch.float32 if mode == 3 else torch.bfloat16)
+    _lib.check(_lib.lib().lp_gemm_bf16_epi(C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), C.c_void_p(bias.data_ptr()),
+                                           C.c_void_p(gate.data_ptr()), C.c_void_p(D.data_ptr()), M, N, K, mode,
+                                           C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    y = A.float() @ B.float().t() + bias
+    ref = {0: y, 1: torch.nn.functional.gelu(y, approximate="tanh"), 2: x0 + gate * y, 3: y}[mode]
+    err = (D.float() - ref).abs().max().item()
+    assert err <= 2e-2 * ref.abs().max().item() + 1e-2, err
+
+
 def _attn(q, k, v, scale):
     B, S, H, _ = q.shape
     Skv = k.shape[1]

@@ -340,30 +340,42 @@ __device__ __forceinline__ void epi_chunk_smem(const GemmEpilogue& ep, int col0,
 // kernel), both CTAs' loads complete on the leader's full barrier, and commits are
 // multicast to both CTAs.  Each CTA's TMEM holds its 128 accumulator rows.
 // ---------------------------------------------------------------------------
-template <int BN>
-constexpr int gemm2_stages() { return BN == 256 ? 6 : 8; }
-template <int BN>
+// Epilogue staging boxes per warp: the fp32 residual epilogue keeps NB = 4 (two residual
+// loads in flight ahead of the chunk being combined) and gives up one mainloop stage for it.
+#ifndef LP_EPI_RESID_BOXES
+#define LP_EPI_RESID_BOXES 4
+#endif
+#ifndef LP_EPI_RESID_DIST
+#define LP_EPI_RESID_DIST 2
+#endif
+template <int MODE>
+constexpr int epi_boxes() { return kEpiTma ? (MODE == EPI_F32_RESID ? LP_EPI_RESID_BOXES : 2) : 0; }
+template <int BN, int MODE = EPI_BF16>
+constexpr int gemm2_stages() { return (BN == 256 ? 6 : 8) - (epi_boxes<MODE>() > 2 ? (BN == 256 ? 1 : 2) : 0); }
+template <int BN, int MODE>
 constexpr int gemm2_smem_bytes() {
-    return gemm2_stages<BN>() * (kBM * kBK * 2 + (BN / 2) * kBK * 2) + 1024 + 256 + (kEpiTma ? 8 * kEpiBox : 0);
+    return gemm2_stages<BN, MODE>() * (kBM * kBK * 2 + (BN / 2) * kBK * 2) + 1024 + 512 +
+           4 * epi_boxes<MODE>() * kEpiBox;
 }
 
 template <int BN, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
             const __grid_constant__ CUtensorMap tmo, GemmEpilogue ep, int M, int N, int K) {
-    constexpr int S = gemm2_stages<BN>();
+    constexpr int S = gemm2_stages<BN, MODE>();
+    constexpr int NB = epi_boxes<MODE>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int A_BYTES = kBM * kBK * 2, B_BYTES = (BN / 2) * kBK * 2;
     uint8_t* sA = smem;
     uint8_t* sB = smem + S * A_BYTES;
-    uint8_t* sE = sB + S * B_BYTES;  // [4 epilogue warps][2][kEpiBox] (1024-aligned)
-    uint64_t* full = reinterpret_cast<uint64_t*>(sE + (kEpiTma ? 8 * kEpiBox : 0));
+    uint8_t* sE = sB + S * B_BYTES;  // [4 epilogue warps][NB][kEpiBox] (1024-aligned)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sE + 4 * NB * kEpiBox);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
-    uint64_t* ebar = tempty + 2;  // [4 warps][2] residual-box loads
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 8);
+    uint64_t* ebar = tempty + 2;  // [4 warps][4] residual-box loads
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 16);
 
     const uint32_t warp = warp_id(), lane = lane_id();
     const uint32_t rank = cluster_ctarank();
@@ -382,7 +394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 256);  // both CTAs' epilogue threads arrive on the leader's
         }
-        for (int b = 0; b < 8; ++b) mbar_init(&ebar[b], 1);
+        for (int b = 0; b < 16; ++b) mbar_init(&ebar[b], 1);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc_2sm(tmem_slot, 2 * BN);
@@ -444,23 +456,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
     } else if (kEpiTma) {
         const uint32_t q = warp & 3;
-        uint8_t* boxes = sE + q * 2 * kEpiBox;
-        uint64_t* wbar = ebar + q * 2;
+        uint8_t* boxes = sE + q * NB * kEpiBox;
+        uint64_t* wbar = ebar + q * 4;
         constexpr int NCH = BN / 32;
         constexpr bool RESID = MODE == EPI_F32_RESID;
-        uint32_t lph[2] = {0, 0};
-        // chunk sequence u = (tile it, chunk c) in order; the residual box of u+1 is loaded
-        // while u is combined.  Buffer of u = u & 1.
-        auto issue_load = [&](int t, int c, int b) {
+        constexpr int DIST = RESID ? LP_EPI_RESID_DIST : 0;  // residual loads in flight ahead of the chunk combined
+        static_assert(!RESID || (DIST >= 1 && DIST < NB), "residual lookahead must fit the boxes");
+        uint32_t lph[4] = {0, 0, 0, 0};
+        // chunk sequence u = (tile, chunk) in processing order, buffer u % NB.  Residual boxes
+        // are TMA-loaded DIST chunks ahead (the load cursor runs across tiles); a buffer is
+        // reloaded once the store from it (chunk u - NB + DIST... = u-2) has been read.
+        int lt = cluster, lc = 0, lu = 0;
+        auto issue_next = [&]() {
+            if (lt >= tiles) return;
+            const int b = lu % NB;
             if (lane == 0) {
-                bulk_wait_read<0>();  // the store that last read buffer b (chunk u-1) is done
+                bulk_wait_read<(NB - DIST - 1 > 0 ? NB - DIST - 1 : 0)>();  // the last store from buffer b has been read
                 mbar_arrive_expect_tx(&wbar[b], kEpiBox);
-                tma_load_2d_cta(&tmo, &wbar[b], boxes + b * kEpiBox, (t % num_n) * BN + c * 32,
-                                (t / num_n) * 2 * kBM + rank * kBM + q * 32);
+                tma_load_2d_cta(&tmo, &wbar[b], boxes + b * kEpiBox, (lt % num_n) * BN + lc * 32,
+                                (lt / num_n) * 2 * kBM + rank * kBM + q * 32);
             }
+            if (++lc == NCH) {
+                lc = 0;
+                lt += nclusters;
+            }
+            ++lu;
         };
+        if (RESID)
+            for (int d = 0; d < DIST; ++d) issue_next();
         int u = 0;
-        if (RESID && cluster < tiles) issue_load(cluster, 0, 0);
         int it = 0;
         for (int t = cluster; t < tiles; t += nclusters, ++it) {
             const int mb = t / num_n, nb = t % num_n;
@@ -472,13 +496,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             const uint32_t taddr = tmem + ((q * 32) << 16) + acc * BN;
 #pragma unroll 1
             for (int c = 0; c < NCH; ++c, ++u) {
-                const int b = u & 1;
+                const int b = u % NB;
                 uint32_t r[32];
                 tmem_ld32(taddr + c * 32, r);
                 if (RESID) {
-                    // next chunk's residual box (may belong to the next tile)
-                    if (c + 1 < NCH) issue_load(t, c + 1, b ^ 1);
-                    else if (t + nclusters < tiles) issue_load(t + nclusters, 0, b ^ 1);
+                    issue_next();  // chunk u + DIST
                     mbar_wait(&wbar[b], lph[b]);
                     lph[b] ^= 1;
                 } else if (lane == 0) {
@@ -559,7 +581,7 @@ static void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const Gem
                          cudaStream_t st) {
     const CUtensorMap to = make_tmap_epi(ep.out, MODE >= EPI_F32_RESID, static_cast<uint64_t>(N), static_cast<uint64_t>(M),
                                          static_cast<uint64_t>(ep.ldo));
-    constexpr int smem = gemm2_smem_bytes<BN>();
+    constexpr int smem = gemm2_smem_bytes<BN, MODE>();
     static bool attr = false;
     if (!attr) {
         LP_CUDA(cudaFuncSetAttribute(k_gemm2<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -308,8 +308,11 @@ __global__ void k_rope_table(float2* __restrict__ tab, int nf, int nh, int nw) {
 // q and k (NSEC = 2 sections of width d at col0 and col0 + d, gains g0 / g1) or one
 // section: RMSNorm over d then 3-D RoPE from the table, in place.  One warp per
 // (row, section); each lane moves 16-byte chunks (8 bf16 = 4 rotation pairs).
+#ifndef LP_RMS_MINB
+#define LP_RMS_MINB 4  // blocks per SM: 64 registers, 32 warps resident (77 registers / 24 warps unconstrained)
+#endif
 template <int PER8>
-__global__ void __launch_bounds__(256) k_rmsnorm_rope_tab(__nv_bfloat16* __restrict__ buf, int64_t rows, int64_t ld,
+__global__ void __launch_bounds__(256, LP_RMS_MINB) k_rmsnorm_rope_tab(__nv_bfloat16* __restrict__ buf, int64_t rows, int64_t ld,
                                                           int64_t col0, int nsec, const float* __restrict__ g0,
                                                           const float* __restrict__ g1, float eps,
                                                           const float2* __restrict__ tab, int64_t rows_per_batch,
@@ -322,18 +325,19 @@ __global__ void __launch_bounds__(256) k_rmsnorm_rope_tab(__nv_bfloat16* __restr
     if (row >= rows) return;
     uint4* p = reinterpret_cast<uint4*>(buf + row * ld + col0 + static_cast<int64_t>(sec) * d);
     const float* g = sec ? g1 : g0;
-    float v[8 * PER8];
+    // the row stays in registers as packed bf16 (4 words per 16-B vector, half the registers
+    // of unpacked floats: more warps resident, more loads in flight) and is unpacked twice
+    uint4 raw[PER8];
+#pragma unroll
+    for (int i = 0; i < PER8; ++i) raw[i] = p[lane + 32 * i];
     float ss = 0.f;
 #pragma unroll
     for (int i = 0; i < PER8; ++i) {
-        const uint4 q = p[lane + 32 * i];
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[u]);
-            v[8 * i + 2 * u] = __bfloat162float(h.x);
-            v[8 * i + 2 * u + 1] = __bfloat162float(h.y);
-            ss += v[8 * i + 2 * u] * v[8 * i + 2 * u] + v[8 * i + 2 * u + 1] * v[8 * i + 2 * u + 1];
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[u]));
+            ss += f.x * f.x + f.y * f.y;
         }
     }
 #pragma unroll
@@ -350,10 +354,12 @@ __global__ void __launch_bounds__(256) k_rmsnorm_rope_tab(__nv_bfloat16* __restr
         const int e = 8 * (lane + 32 * i);
         const float4 ga = reinterpret_cast<const float4*>(g + e)[0], gb = reinterpret_cast<const float4*>(g + e)[1];
         const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+        const uint32_t in[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
         uint32_t w[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            float a = v[8 * i + 2 * u] * r * gv[2 * u], b = v[8 * i + 2 * u + 1] * r * gv[2 * u + 1];
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&in[u]));
+            float a = f.x * r * gv[2 * u], b = f.y * r * gv[2 * u + 1];
             if (tab) {
                 const int j = ((e & 127) >> 1) + u;  // pair within the head
                 const float2 cs = j < 22 ? tf[j] : (j < 43 ? th[j] : tw[j]);

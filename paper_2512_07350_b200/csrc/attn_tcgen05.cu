@@ -34,6 +34,17 @@ constexpr int kAtom = 128 * 128;       // one [128 rows x 128 B] swizzle block
 constexpr int kTileBytes = 2 * kAtom;  // [128 x 128] bf16 = 32 KB
 constexpr int kKStages = 3, kVStages = 2;
 constexpr int kAttnSmem = (2 /*Q0,Q1*/ + kKStages + kVStages) * kTileBytes + 1024 + 256;
+#ifndef LP_ATTN_O_LSU
+constexpr bool kAttnOTma = true;  // O epilogue: staged in Q's smem, TMA tensor stores
+#else
+constexpr bool kAttnOTma = false;  // A/B build: thread-per-row 16-B stores
+#endif
+__device__ __forceinline__ void tma_store_3d(const void* tmap, const void* smem, int32_t c0, int32_t c1, int32_t c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
 
 struct AttnKernelArgs {
     int64_t q_col0, k_col0, v_col0;
@@ -188,7 +199,7 @@ __device__ __forceinline__ void softmax_block(uint32_t tS, uint32_t tO, int vali
 template <int POLY, bool TR = false>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     k_attention(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
-                const __grid_constant__ CUtensorMap tv, AttnKernelArgs a) {
+                const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap to, AttnKernelArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;                          // [tile][2 atoms]
@@ -385,9 +396,44 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tc_fence_after();
         const int64_t grow = static_cast<int64_t>(qt) * 2 * kTile + t * kTile + row;
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-        __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.o) + (b * a.q_rows_per_batch + grow) * a.ldo + h * kHD;
+        if (kAttnOTma) {
+            // O_t through Q_t's shared memory (dead: Q_t's last S MMA completed before its
+            // last PV, which o_final follows), in the same 128B-swizzled [128 rows x 64 col]
+            // atoms; each warp then TMA-stores its 32 rows as two 64-column boxes.  The 3-D O
+            // map clips rows >= n_q per batch.
+            uint8_t* stage = sQ + t * kTileBytes;
+#pragma unroll 1
+            for (int cc = 0; cc < kHD; cc += 32) {
+                uint32_t r[32];
+                tmem_ld32(tO + cc, r);
+                tmem_ld_wait();
+                uint8_t* arow = stage + (cc >> 6) * kAtom + row * 128;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int unit = ((cc & 63) >> 3) + u;
+                    *reinterpret_cast<uint4*>(arow + ((unit ^ (row & 7)) << 4)) =
+                        make_uint4(pack_bf16(__uint_as_float(r[8 * u + 0]) * inv, __uint_as_float(r[8 * u + 1]) * inv),
+                                   pack_bf16(__uint_as_float(r[8 * u + 2]) * inv, __uint_as_float(r[8 * u + 3]) * inv),
+                                   pack_bf16(__uint_as_float(r[8 * u + 4]) * inv, __uint_as_float(r[8 * u + 5]) * inv),
+                                   pack_bf16(__uint_as_float(r[8 * u + 6]) * inv, __uint_as_float(r[8 * u + 7]) * inv));
+                }
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                const int32_t r0 = static_cast<int32_t>(qt * 2 * kTile + t * kTile + q * 32);
+                for (int at = 0; at < 2; ++at)
+                    tma_store_3d(&to, stage + at * kAtom + q * 32 * 128, static_cast<int32_t>(h * kHD + at * 64), r0, b);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                // only the smem READ must finish before the CTA retires (its smem is released);
+                // the global writes complete asynchronously and are visible at grid end
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
+            __syncwarp();
+        } else
 #pragma unroll 1
         for (int cc = 0; cc < kHD; cc += 32) {
+            __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.o) + (b * a.q_rows_per_batch + grow) * a.ldo + h * kHD;
             uint32_t r[32];
             tmem_ld32(tO + cc, r);
             tmem_ld_wait();
@@ -413,6 +459,9 @@ static int attn_poly() {
     return v == 0 || v == 6 || v == 8 ? v : 4;
 }
 
+CUtensorMap make_tmap_3d_bf16(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
+                              uint32_t b0, uint32_t b1, uint32_t b2);  // gemm_tcgen05.cu (128B swizzle)
+
 void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
@@ -430,6 +479,8 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     const CUtensorMap tq = make_tmap_2d_bf16(x.q, x.ldq, x.q_total_rows, x.ldq * 2, 64, kTile);
     const CUtensorMap tk = make_tmap_2d_bf16(x.k, x.ldk, x.kv_total_rows, x.ldk * 2, 64, kTile);
     const CUtensorMap tv = make_tmap_2d_bf16(x.v, x.ldv, x.kv_total_rows, x.ldv * 2, 64, kTile);
+    // O as [batch][n_q rows][ldo]: rows past n_q of a batch are clipped by the map
+    const CUtensorMap to = make_tmap_3d_bf16(x.o, x.ldo, x.n_q, x.batch, x.ldo * 2, x.q_rows_per_batch * x.ldo * 2, 64, 32, 1);
     AttnKernelArgs a;
     a.q_col0 = x.q_col0;
     a.k_col0 = x.k_col0;
@@ -445,13 +496,13 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     const int cls = x.n_kv == x.n_q && x.q == x.k ? KC_SELF_ATTN : KC_CROSS_ATTN;
     prof_begin(cls, st);
     switch (tune_get("attn_trace", 0) ? -tune_get("attn_trace", 0) : attn_poly()) {
-        case -1: k_attention<0, true><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
-        case -2: k_attention<-1, true><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
-        case -3: k_attention<-2, true><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
-        case 0: k_attention<0><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
-        case 6: k_attention<6><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
-        case 8: k_attention<8><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
-        default: k_attention<4><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, a); break;
+        case -1: k_attention<0, true><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, to, a); break;
+        case -2: k_attention<-1, true><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, to, a); break;
+        case -3: k_attention<-2, true><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, to, a); break;
+        case 0: k_attention<0><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, to, a); break;
+        case 6: k_attention<6><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, to, a); break;
+        case 8: k_attention<8><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, to, a); break;
+        default: k_attention<4><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, to, a); break;
     }
     LP_LAUNCH_CHECK();
     prof_end(cls, st, 4.0 * x.batch * x.heads * static_cast<double>(x.n_q) * static_cast<double>(x.n_kv) * kHD,

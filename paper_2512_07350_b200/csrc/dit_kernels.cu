@@ -308,69 +308,110 @@ __global__ void k_rope_table(float2* __restrict__ tab, int nf, int nh, int nw) {
 // q and k (NSEC = 2 sections of width d at col0 and col0 + d, gains g0 / g1) or one
 // section: RMSNorm over d then 3-D RoPE from the table, in place.  One warp per
 // (row, section); each lane moves 16-byte chunks (8 bf16 = 4 rotation pairs).
+// x / d for 32-bit x < 2^31 by multiply-shift (Granlund-Montgomery; exact in that range)
+struct RopeDiv {
+    uint64_t mul;
+    uint32_t shift, d;
+};
+struct RopeDivs {
+    RopeDiv batch, w, h;
+};
+static RopeDiv make_rdiv(uint32_t d) {
+    if (d == 0) d = 1;
+    RopeDiv r;
+    r.d = d;
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    r.shift = 31 + l;
+    r.mul = ((1ull << r.shift) + d - 1) / d;
+    return r;
+}
+__device__ __forceinline__ uint32_t rdiv(uint32_t x, const RopeDiv& v) {
+    return static_cast<uint32_t>((static_cast<uint64_t>(x) * v.mul) >> v.shift);
+}
+
 #ifndef LP_RMS_MINB
-#define LP_RMS_MINB 4  // blocks per SM: 64 registers, 32 warps resident (77 registers / 24 warps unconstrained)
+#define LP_RMS_MINB 2  // blocks per SM of the persistent grid (ncu A/B: 2 -> 72.0 us, 3 -> 82.2, 4 -> 115.5)
 #endif
 template <int PER8>
 __global__ void __launch_bounds__(256, LP_RMS_MINB) k_rmsnorm_rope_tab(__nv_bfloat16* __restrict__ buf, int64_t rows, int64_t ld,
                                                           int64_t col0, int nsec, const float* __restrict__ g0,
                                                           const float* __restrict__ g1, float eps,
-                                                          const float2* __restrict__ tab, int64_t rows_per_batch,
+                                                          const float2* __restrict__ tab, const RopeDivs dv,
                                                           int nf, int nh, int nw) {
     constexpr int d = PER8 * 256;
-    const int64_t wid = blockIdx.x * 8LL + threadIdx.x / 32;
+    // 32-bit index math with multiply-shift division (the host checks the ranges): the
+    // former 64-bit div/mod sequences cost more issue slots than the row's arithmetic.
+    // Persistent warps walk (row, section) units with a stride of all warps, and the next
+    // unit's row is loaded before the current one is normalised and rotated.
+    const uint32_t nwarps = gridDim.x * 8u, units = static_cast<uint32_t>(rows) * static_cast<uint32_t>(nsec);
     const int lane = threadIdx.x & 31;
-    const int64_t row = wid / nsec;
-    const int sec = static_cast<int>(wid % nsec);
-    if (row >= rows) return;
-    uint4* p = reinterpret_cast<uint4*>(buf + row * ld + col0 + static_cast<int64_t>(sec) * d);
-    const float* g = sec ? g1 : g0;
-    // the row stays in registers as packed bf16 (4 words per 16-B vector, half the registers
-    // of unpacked floats: more warps resident, more loads in flight) and is unpacked twice
-    uint4 raw[PER8];
+    uint32_t wid = blockIdx.x * 8u + threadIdx.x / 32;
+    auto unit_ptr = [&](uint32_t w) {
+        const uint32_t row = nsec == 2 ? w >> 1 : w;
+        const int sec = nsec == 2 ? static_cast<int>(w & 1u) : 0;
+        return reinterpret_cast<uint4*>(buf + static_cast<int64_t>(row) * ld + col0 + static_cast<int64_t>(sec) * d);
+    };
+    uint4 raw[PER8], nxt[PER8];
+    if (wid < units) {
+        const uint4* p0 = unit_ptr(wid);
 #pragma unroll
-    for (int i = 0; i < PER8; ++i) raw[i] = p[lane + 32 * i];
-    float ss = 0.f;
-#pragma unroll
-    for (int i = 0; i < PER8; ++i) {
-        const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[u]));
-            ss += f.x * f.x + f.y * f.y;
-        }
+        for (int i = 0; i < PER8; ++i) nxt[i] = p0[lane + 32 * i];
     }
+    for (; wid < units; wid += nwarps) {
+        const uint32_t row = nsec == 2 ? wid >> 1 : wid;
+        const int sec = nsec == 2 ? static_cast<int>(wid & 1u) : 0;
+        uint4* p = unit_ptr(wid);
+        const float* g = sec ? g1 : g0;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
-    const float r = rsqrtf(ss / d + eps);
-    const int64_t tok = row % rows_per_batch;
-    const int px = static_cast<int>(tok % nw), py = static_cast<int>((tok / nw) % nh),
-              pf = static_cast<int>(tok / (static_cast<int64_t>(nw) * nh));
-    const float2* tf = tab + pf * 22;
-    const float2* th = tab + nf * 22 + py * 21 - 22;
-    const float2* tw = tab + nf * 22 + nh * 21 + px * 21 - 43;
+        for (int i = 0; i < PER8; ++i) raw[i] = nxt[i];
+        if (wid + nwarps < units) {
+            const uint4* pn = unit_ptr(wid + nwarps);
 #pragma unroll
-    for (int i = 0; i < PER8; ++i) {
-        const int e = 8 * (lane + 32 * i);
-        const float4 ga = reinterpret_cast<const float4*>(g + e)[0], gb = reinterpret_cast<const float4*>(g + e)[1];
-        const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
-        const uint32_t in[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
-        uint32_t w[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&in[u]));
-            float a = f.x * r * gv[2 * u], b = f.y * r * gv[2 * u + 1];
-            if (tab) {
-                const int j = ((e & 127) >> 1) + u;  // pair within the head
-                const float2 cs = j < 22 ? tf[j] : (j < 43 ? th[j] : tw[j]);
-                const float a2 = a * cs.x - b * cs.y, b2 = a * cs.y + b * cs.x;
-                a = a2;
-                b = b2;
-            }
-            const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-            w[u] = *reinterpret_cast<const uint32_t*>(&h);
+            for (int i = 0; i < PER8; ++i) nxt[i] = pn[lane + 32 * i];
         }
-        p[lane + 32 * i] = make_uint4(w[0], w[1], w[2], w[3]);
+        float ss = 0.f;
+#pragma unroll
+        for (int i = 0; i < PER8; ++i) {
+            const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[u]));
+                ss += f.x * f.x + f.y * f.y;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+        const float r = rsqrtf(ss / d + eps);
+        const uint32_t tok = row - rdiv(row, dv.batch) * dv.batch.d;
+        const uint32_t tw_ = rdiv(tok, dv.w), pf = rdiv(tw_, dv.h);
+        const int px = static_cast<int>(tok - tw_ * dv.w.d), py = static_cast<int>(tw_ - pf * dv.h.d);
+        const float2* tf = tab + static_cast<int>(pf) * 22;
+        const float2* th = tab + nf * 22 + py * 21 - 22;
+        const float2* tw = tab + nf * 22 + nh * 21 + px * 21 - 43;
+#pragma unroll
+        for (int i = 0; i < PER8; ++i) {
+            const int e = 8 * (lane + 32 * i);
+            const float4 ga = reinterpret_cast<const float4*>(g + e)[0], gb = reinterpret_cast<const float4*>(g + e)[1];
+            const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+            const uint32_t in[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
+            uint32_t w[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&in[u]));
+                float a = f.x * r * gv[2 * u], b = f.y * r * gv[2 * u + 1];
+                if (tab) {
+                    const int j = ((e & 127) >> 1) + u;  // pair within the head
+                    const float2 cs = j < 22 ? tf[j] : (j < 43 ? th[j] : tw[j]);
+                    const float a2 = a * cs.x - b * cs.y, b2 = a * cs.y + b * cs.x;
+                    a = a2;
+                    b = b2;
+                }
+                const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+                w[u] = *reinterpret_cast<const uint32_t*>(&h);
+            }
+            p[lane + 32 * i] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
     }
 }
 
@@ -383,12 +424,22 @@ void rope_table(float2* tab, int nf, int nh, int nw, cudaStream_t st) {
 bool rmsnorm_rope_tab(__nv_bfloat16* buf, int64_t rows, int64_t ld, int64_t col0, int d, int nsec, const float* g0,
                       const float* g1, float eps, const float2* tab, int64_t rows_per_batch, int nf, int nh, int nw,
                       cudaStream_t st) {
-    if (d % 256 || (ld % 8) || (col0 % 8)) return false;
-    const unsigned gr = static_cast<unsigned>((rows * nsec + 7) / 8);
+    if (d % 256 || (ld % 8) || (col0 % 8) || (nsec != 1 && nsec != 2)) return false;
+    if (rows * nsec >= (1ll << 31) || rows_per_batch >= (1ll << 31)) return false;
+    RopeDivs dv;
+    dv.batch = make_rdiv(static_cast<uint32_t>(rows_per_batch));
+    dv.w = make_rdiv(static_cast<uint32_t>(nw));
+    dv.h = make_rdiv(static_cast<uint32_t>(nh));
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const unsigned gr = static_cast<unsigned>(std::min<int64_t>((rows * nsec + 7) / 8, static_cast<int64_t>(sms) * LP_RMS_MINB));
 #define LP_RMT(P)                                                                                                   \
     if (d == 256 * P) {                                                                                             \
-        k_rmsnorm_rope_tab<P><<<gr, 256, 0, st>>>(buf, rows, ld, col0, nsec, g0, g1, eps, tab, rows_per_batch, nf, nh, \
-                                                  nw);                                                              \
+        k_rmsnorm_rope_tab<P><<<gr, 256, 0, st>>>(buf, rows, ld, col0, nsec, g0, g1, eps, tab, dv, nf, nh, nw);    \
         LP_LAUNCH_CHECK();                                                                                          \
         return true;                                                                                                \
     }

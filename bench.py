@@ -325,6 +325,16 @@ def run_ours(args, rank, world, local_rank):
     assert torch.isfinite(zout).all(), "non-finite latent"
     if lp.device_flags(reset=True) & 4:
         raise SystemExit(f"rank {rank}: peer exchange watchdog fired (a peer's epoch flag never arrived)")
+    if world > 1:
+        # z is replicated: every rank must hold the same bits after the exchanges (catches a
+        # broken exchange that still yields finite numbers)
+        chk = torch.tensor([int(eng.z.data.view(torch.int32).to(torch.int64).sum().item())], dtype=torch.int64,
+                           device="cpu" if GLOO_TEST else "cuda")
+        lo, hi = chk.clone(), chk.clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        if int(lo.item()) != int(hi.item()):
+            raise SystemExit(f"rank {rank}: replicated latent differs across ranks after the run")
 
     # ---- per-kernel roofline pass: one rotation cycle (T, H, W) with the shard streams
     # serialised, so each kernel's CUDA-event duration is its own (in the timed region two

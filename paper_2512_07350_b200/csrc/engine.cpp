@@ -476,6 +476,7 @@ int lp_engine_step_phase(lp_engine* e, int32_t step, int32_t phase, void* stream
     return guard([&] {
         cudaStream_t st = as_stream(stream);
         const uint64_t l0 = launch_count();
+        if (e->peer) fail(LP_ERR_INVALID_ARGUMENT, "peer-attached engines exchange inside lp_engine_run");
         if (phase == 1) {
             if (e->M > 1 && !e->comm)
                 fail(LP_ERR_INVALID_GROUPING, "hybrid engine without NCCL: drive its stages with lp_engine_stage");

@@ -96,8 +96,8 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
         e->M = c->group_size > 1 ? c->group_size : 1;
         e->groups = c->world;  // plain LP: every rank is its own group
         if (e->M > 1) {
-            if (!c->dit) { delete e; fail(LP_ERR_INVALID_GROUPING, "hybrid groups need the DiT denoiser"); }
             if (c->world % e->M) { delete e; fail(LP_ERR_INVALID_GROUPING, "world must be a multiple of group_size"); }
+            if (!c->dit) { delete e; fail(LP_ERR_INVALID_GROUPING, "hybrid groups need the DiT denoiser"); }
             int L = 0;
             {
                 lp_dit_config dc;

@@ -119,6 +119,15 @@ def test_hybrid_config_validation():
     from paper_2512_07350_b200 import lp
 
     z, cond = lp.synthetic_latent_host(DIMS, 4, 2025)
-    with pytest.raises(lp.LpError):  # toy denoisers cannot be pipelined
+    with pytest.raises(lp.LpError, match="DiT"):  # toy denoisers cannot be pipelined
         lp.LpEngine(DIMS, PATCH, 4, 2, 0.5, STEPS, 0.05, 5.0, list(cond), denoiser="box", world=2, rank=0,
+                    group_size=2)
+
+
+def test_hybrid_world_must_divide():
+    from paper_2512_07350_b200 import lp
+
+    z, cond = lp.synthetic_latent_host(DIMS, 4, 2025)
+    with pytest.raises(lp.LpError, match="multiple of group_size"):  # checked before any device work
+        lp.LpEngine(DIMS, PATCH, 4, 1, 0.0, STEPS, 0.05, 5.0, list(cond), denoiser="box", world=3, rank=0,
                     group_size=2)

@@ -9,6 +9,8 @@ latents within a stated bf16/fp32 tolerance per step and after the full schedule
   Denoiser slot, traced after every step, vs our engine stepped one timestep at a time.
   Per step i: rel. L2 of (z_i - z_0) <= 1.5e-2 and max |dz_i| <= 5e-3 + 1e-3 * i; the ledger
   bytes are equal. Schedules: C1 (4 steps, K=2), 12 steps K=4, and 50 steps K=2 (C2's T).
+* Full size: one LP step of C2 itself (16x21x60x104, K=4, 30 blocks) vs the reference run_lp
+  driving the fp32 DiT.
 """
 import os
 
@@ -79,5 +81,37 @@ def test_lp_dit_loop_per_step_tolerance(cuda, reference, dims, K, steps):
         worst.append((i, rel, mx))
         assert np.isfinite(rel) and rel <= 1.5e-2, (i, rel)
         assert mx <= 5e-3 + 1e-3 * i, (i, mx)
+    assert eng.comm()["ledger_bytes"] == ledger
+    eng.close()
+
+
+def test_c2_full_size_lp_step_matches_reference_run_lp(cuda, reference):
+    """BASELINE configs[1] at full size: one LP step of the C2 workload (16x21x60x104 f32,
+    K=4, r=0.5, w=5, 30-block WAN-1.3B-shaped DiT).  The UNMODIFIED reference run_lp drives
+    the fp32 DiT through its Denoiser slot (8 full-size fp32 forwards: 4 shards x 2 CFG
+    passes); our engine runs the same step with bf16 tcgen05 kernels.  Tolerance as above:
+    rel. L2 of the update <= 1.5e-2, max |dz| <= 6e-3; ledgers equal."""
+    from tests.dit_reference import DiTReference
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    dims, K, r, eta, w = (16, 21, 60, 104), 4, 0.5, 0.05, 5.0
+    z, cond = lp.synthetic_latent(dims, 4, 2025)
+    dit = lp.DiTDenoiser(cond)
+    ck, cv = _ctx(dit)
+    ref = DiTReference(dit)
+
+    def predict(zz, t, c, is_null):
+        return ref.predict(torch.from_numpy(zz).float().cuda(), t, ck, cv, 0 if is_null else 1).double().cpu().numpy()
+
+    os.environ["LPSIM_THREADS"] = "0"
+    z0 = z.to_numpy()
+    want, ledger = reference.run_lp_callback(predict, z0, 4, 1, eta, w, cond, (1, 2, 2), K, r)
+    eng = lp.LpEngine(dims, (1, 2, 2), 4, K, r, 1, eta, w, cond, denoiser="dit", dit=dit)
+    eng.load(z)
+    eng.run(1, 1)
+    got = eng.z.data.double().cpu().numpy()
+    rel = np.linalg.norm(got - want) / np.linalg.norm(want - z0)
+    assert np.isfinite(rel) and rel <= 1.5e-2, rel
+    assert np.abs(got - want).max() <= 6e-3
     assert eng.comm()["ledger_bytes"] == ledger
     eng.close()

@@ -164,3 +164,29 @@ def test_engine_nccl_exchange_path_single_rank(cuda, oracle, d):
     eng.close()
     assert np.array_equal(got, want)
     assert comm["ledger_bytes"] == ledger and comm["nccl_bytes_received"] == 0
+
+
+@pytest.mark.parametrize("d", [2, 4, 8])
+@pytest.mark.parametrize("shape,patch,k,r,step", [
+    ((4, 9, 16, 24), (1, 2, 2), 4, 0.5, 1),   # T axis, inner = 384: 8-element vector path
+    ((3, 6, 16, 24), (1, 2, 2), 4, 0.5, 2),   # H axis, inner = 24: vector path
+    ((2, 5, 6, 52), (1, 2, 2), 4, 0.5, 3),    # W axis, inner = 1: x-stationary path
+    ((2, 7, 6, 10), (1, 1, 1), 3, 0.25, 2),   # H axis, inner = 10: per-element path
+    ((2, 16, 4, 8), (1, 1, 1), 8, 6.0, 1),    # every position covered by > 4 entries: table fallback
+])
+def test_reconstruct_paths_bitexact(cuda, oracle, shape, patch, k, r, step, d):
+    """K10's code paths (lp_kernels.cu k_reconstruct_cov / k_reconstruct_xs and the fallback),
+    exact mode, against the oracle bit for bit, with and without the fused sampler update."""
+    z, _ = oracle.synthetic(shape, d, 11)
+    plan = lp.build_plan(shape, patch, step, k, r)
+    oplan = oracle.build_plan(shape, patch, step, k, r)
+    rng = np.random.default_rng(7)
+    preds_np = [lp._quantize_np(rng.normal(size=sub_shape(shape, oplan, e)) * 3, d).astype(np.float64)
+                for e in range(oplan.n)]
+    packed = np.concatenate([p.reshape(-1) for p in preds_np])
+    want = oracle.reconstruct(packed, shape, d, oplan)
+    preds = [lp.LatentTensor.from_numpy(p, d) for p in preds_np]
+    assert np.array_equal(lp.reconstruct(preds, plan, shape).to_numpy(), want)
+    zt = lp.LatentTensor.from_numpy(z, d)
+    lp.reconstruct_update(preds, plan, zt, 0.05)
+    assert np.array_equal(zt.to_numpy(), oracle.sampler_step(z, want, d, 0.05))

@@ -17,18 +17,17 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-WORLD = 2
 DIMS = (16, 5, 16, 16)
 PATCH = (1, 2, 2)
-K, R, STEPS = 4, 0.5, 5
+K, R = 4, 0.5
 
 
-def _engine(lp, denoiser, d, cond, world, rank, dit=None):
-    return lp.LpEngine(DIMS, PATCH, d, K, R, STEPS, 0.05, 5.0, list(cond), denoiser=denoiser, radius=(1, 1, 1),
+def _engine(lp, denoiser, d, cond, world, rank, dit=None, steps=5):
+    return lp.LpEngine(DIMS, PATCH, d, K, R, steps, 0.05, 5.0, list(cond), denoiser=denoiser, radius=(1, 1, 1),
                        world=world, rank=rank, dit=dit)
 
 
-def _worker(rank, port, q, denoiser, d):
+def _worker(rank, port, q, denoiser, d, WORLD, STEPS):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=WORLD)
@@ -37,7 +36,7 @@ def _worker(rank, port, q, denoiser, d):
 
         z, cond = lp.synthetic_latent_host(DIMS, d, 2025)
         dit = lp.DiTDenoiser(list(cond), num_layers=2) if denoiser == "dit" else None
-        eng = _engine(lp, denoiser, d, cond, WORLD, rank, dit)
+        eng = _engine(lp, denoiser, d, cond, WORLD, rank, dit, STEPS)
         eng.load(lp.LatentTensor.from_numpy(z, d))
         handles = [None] * WORLD
         dist.all_gather_object(handles, eng.ipc_handle())
@@ -57,11 +56,11 @@ def _worker(rank, port, q, denoiser, d):
         q.put((rank, repr(e), None, None))
 
 
-def _run(denoiser, d):
+def _run(denoiser, d, WORLD=2, STEPS=5):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29600 + (os.getpid() % 1000) + 13 * d
-    procs = [ctx.Process(target=_worker, args=(r, port, q, denoiser, d)) for r in range(WORLD)]
+    port = 29600 + (os.getpid() % 1000) + 13 * d + 3 * WORLD
+    procs = [ctx.Process(target=_worker, args=(r, port, q, denoiser, d, WORLD, STEPS)) for r in range(WORLD)]
     for p in procs:
         p.start()
     res = sorted((q.get(timeout=600) for _ in range(WORLD)), key=lambda x: x[0])
@@ -70,16 +69,17 @@ def _run(denoiser, d):
     for r, out, flags, _ in res:
         assert isinstance(out, bytes), out
         assert flags == 0, f"rank {r} raised device flags {flags} (4 = peer timeout)"
-    assert res[0][1] == res[1][1], "ranks disagree"
+    assert all(r[1] == res[0][1] for r in res), "ranks disagree"
     assert res[0][3]["nccl_bytes_received"] > 0
     return res[0][1]
 
 
 @pytest.mark.gpu
-def test_peer_exchange_toy_bitexact_vs_oracle(cuda, oracle):
-    got = _run("box", 4)
+@pytest.mark.parametrize("world,steps", [(2, 5), (3, 9)])
+def test_peer_exchange_toy_bitexact_vs_oracle(cuda, oracle, world, steps):
+    got = _run("box", 4, world, steps)
     z, cond = oracle.synthetic(DIMS, 4, 2025)
-    want, _ = oracle.run_lp(0, (1, 1, 1), z, 4, STEPS, 0.05, 5.0, cond, PATCH, K, R)
+    want, _ = oracle.run_lp(0, (1, 1, 1), z, 4, steps, 0.05, 5.0, cond, PATCH, K, R)
     assert np.frombuffer(got, np.float32).astype(np.float64).tobytes() == want.tobytes()
 
 
@@ -92,7 +92,7 @@ def test_peer_exchange_dit_equals_single_process(cuda):
     dit = lp.DiTDenoiser(list(cond), num_layers=2)
     eng = _engine(lp, "dit", 4, cond, 1, 0, dit)
     eng.load(lp.LatentTensor.from_numpy(z, 4))
-    eng.run(1, STEPS)
+    eng.run(1, 5)
     want = eng.z.data.cpu().numpy().tobytes()
     eng.close()
     assert got == want

@@ -34,6 +34,17 @@ constexpr int kAtom = 128 * 128;       // one [128 rows x 128 B] swizzle block
 constexpr int kTileBytes = 2 * kAtom;  // [128 x 128] bf16 = 32 KB
 constexpr int kKStages = 3, kVStages = 2;
 constexpr int kAttnSmem = (2 /*Q0,Q1*/ + kKStages + kVStages) * kTileBytes + 1024 + 256;
+// NT = Q tiles per CTA.  NT = 2 (self-attention): the two tiles ping-pong inside the CTA,
+// K/V rings 3/2, 224 KB smem, all 512 TMEM columns, one CTA per SM.  NT = 1 (short key
+// sequences, i.e. cross-attention over 512 text tokens): one tile, single-buffered K/V,
+// 96 KB smem and 256 TMEM columns, so TWO CTAs share an SM and one CTA's fixed costs (Q/K
+// fetch, pipeline ramp, drain, epilogue ~4.6 us, profiles/r2b) overlap the other's blocks.
+template <int NT> struct AttnCfg {
+    static constexpr int KS = NT == 2 ? kKStages : 1, VS = NT == 2 ? kVStages : 1;
+    static constexpr int threads = 64 + 128 * NT;
+    static constexpr int smem = (NT + KS + VS) * kTileBytes + 1024 + 256;
+    static constexpr uint32_t tmem_cols = NT == 2 ? 512 : 256;
+};
 #ifndef LP_ATTN_O_LSU
 constexpr bool kAttnOTma = true;  // O epilogue: staged in Q's smem, TMA tensor stores
 #else
@@ -218,26 +229,27 @@ __device__ __forceinline__ void softmax_block(uint32_t tS, uint32_t tO, int vali
     l_run += ls.x + ls.y;
 }
 
-template <int POLY, bool TR = false>
-__global__ void __launch_bounds__(kAttnThreads, 1)
+template <int POLY, bool TR = false, int NT = 2>
+__global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
     k_attention(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                 const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap to, AttnKernelArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;                          // [tile][2 atoms]
-    uint8_t* sK = sQ + 2 * kTileBytes;           // [kKStages]
-    uint8_t* sV = sK + kKStages * kTileBytes;    // [kVStages]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVStages * kTileBytes);
+    constexpr int KS = AttnCfg<NT>::KS, VS = AttnCfg<NT>::VS;
+    uint8_t* sQ = smem;                    // [tile][2 atoms]
+    uint8_t* sK = sQ + NT * kTileBytes;    // [KS]
+    uint8_t* sV = sK + KS * kTileBytes;    // [VS]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VS * kTileBytes);
     uint64_t* q_full = bars + 0;
-    uint64_t* k_full = bars + 1;    // [kKStages]
-    uint64_t* k_empty = bars + 4;   // [kKStages]
-    uint64_t* v_full = bars + 7;    // [kVStages]
-    uint64_t* v_empty = bars + 9;   // [kVStages]
-    uint64_t* s_full = bars + 11;   // [tile]
-    uint64_t* p_full = bars + 13;   // [tile]
-    uint64_t* p_half = bars + 15;   // [tile]
-    uint64_t* o_final = bars + 17;  // [tile]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
+    uint64_t* k_full = q_full + 1;     // [KS]
+    uint64_t* k_empty = k_full + KS;   // [KS]
+    uint64_t* v_full = k_empty + KS;   // [VS]
+    uint64_t* v_empty = v_full + VS;   // [VS]
+    uint64_t* s_full = v_empty + VS;   // [tile]
+    uint64_t* p_full = s_full + NT;    // [tile]
+    uint64_t* p_half = p_full + NT;    // [tile]
+    uint64_t* o_final = p_half + NT;   // [tile]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + NT);
 
     const uint32_t warp = warp_id(), lane = lane_id();
     const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -248,15 +260,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tma_prefetch(&tk);
         tma_prefetch(&tv);
         mbar_init(q_full, 1);
-        for (int s = 0; s < kKStages; ++s) {
+        for (int s = 0; s < KS; ++s) {
             mbar_init(&k_full[s], 1);
             mbar_init(&k_empty[s], 1);
         }
-        for (int s = 0; s < kVStages; ++s) {
+        for (int s = 0; s < VS; ++s) {
             mbar_init(&v_full[s], 1);
             mbar_init(&v_empty[s], 1);
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < NT; ++s) {
             mbar_init(&s_full[s], 1);
             mbar_init(&p_full[s], 128);
             mbar_init(&p_half[s], 128);
@@ -264,7 +276,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    if (warp == 2) tmem_alloc(tmem_slot, AttnCfg<NT>::tmem_cols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -273,18 +285,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     if (warp == 0) {
         if (lane == 0) {
             // K runs ahead in a 3-deep ring (needed first, by S = Q K^T); V in a 2-deep ring
-            const int32_t qrow = static_cast<int32_t>(b * a.q_rows_per_batch + qt * 2 * kTile);
+            const int32_t qrow = static_cast<int32_t>(b * a.q_rows_per_batch + qt * NT * kTile);
             const int32_t qc = static_cast<int32_t>(a.q_col0 + h * kHD);
-            mbar_arrive_expect_tx(q_full, 2 * kTileBytes);
-            for (int t = 0; t < 2; ++t) {
+            mbar_arrive_expect_tx(q_full, NT * kTileBytes);
+            for (int t = 0; t < NT; ++t) {
                 tma_load_2d(&tq, q_full, sQ + t * kTileBytes, qc, qrow + t * kTile);
                 tma_load_2d(&tq, q_full, sQ + t * kTileBytes + kAtom, qc + 64, qrow + t * kTile);
             }
             const int32_t kc = static_cast<int32_t>(a.k_col0 + h * kHD), vc = static_cast<int32_t>(a.v_col0 + h * kHD);
             auto load_k = [&](int j) {
-                const int s = j % kKStages;
-                mbar_wait(&k_empty[s], ((j / kKStages) & 1) ^ 1);
-                if (POLY == -2 && j >= kKStages) {  // debug (attn_trace=3): no TMA once the ring is primed
+                const int s = j % KS;
+                mbar_wait(&k_empty[s], ((j / KS) & 1) ^ 1);
+                if (POLY == -2 && j >= KS) {  // debug (attn_trace=3): no TMA once the ring is primed
                     mbar_arrive(&k_full[s]);
                     return;
                 }
@@ -294,9 +306,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 tma_load_2d(&tk, &k_full[s], sK + s * kTileBytes + kAtom, kc + 64, kr);
             };
             auto load_v = [&](int j) {
-                const int s = j % kVStages;
-                mbar_wait(&v_empty[s], ((j / kVStages) & 1) ^ 1);
-                if (POLY == -2 && j >= kVStages) {
+                const int s = j % VS;
+                mbar_wait(&v_empty[s], ((j / VS) & 1) ^ 1);
+                if (POLY == -2 && j >= VS) {
                     mbar_arrive(&v_full[s]);
                     return;
                 }
@@ -306,10 +318,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 tma_load_2d(&tv, &v_full[s], sV + s * kTileBytes + kAtom, vc + 64, kr);
             };
             int jk = 0;
-            for (; jk < nkv && jk < kKStages - 1; ++jk) load_k(jk);
+            for (; jk < nkv && jk < KS - 1; ++jk) load_k(jk);
             for (int j = 0; j < nkv; ++j) {
+                // single-buffered K (NT = 1): K_j first — S_j needs it before PV_j needs V_j
+                if (KS == 1 && jk < nkv) load_k(jk++);
                 load_v(j);
-                if (jk < nkv) load_k(jk++);
+                if (KS > 1 && jk < nkv) load_k(jk++);
             }
         }
     } else if (warp == 1) {
@@ -331,9 +345,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             const uint64_t dV = desc_sw128(smem_u32(sV), /*sbo=*/1024, /*lbo=*/kAtom);
             wait1(q_full, 0);
             auto issue_s = [&](int t, int j) {
-                const int s = j % kKStages;
+                const int s = j % KS;
                 if (t == 0) {
-                    wait1(&k_full[s], (j / kKStages) & 1);
+                    wait1(&k_full[s], (j / KS) & 1);
                     tc_fence_after();
                 }
                 if (leader) {
@@ -344,30 +358,29 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                         mma_ss(tmem + t * 128, q0 + off, k0 + off, idS, k != 0);
                     }
                     mma_commit(&s_full[t]);
-                    if (t == 1) mma_commit(&k_empty[s]);  // both tiles' S issued: K_j slot frees on completion
+                    if (t == NT - 1) mma_commit(&k_empty[s]);  // every tile's S issued: K_j slot frees on completion
                 }
                 __syncwarp();
             };
             auto issue_pv = [&](int t, int j, int half) {
                 if (leader) {
-                    const uint64_t v0 = dV + (j % kVStages) * (kTileBytes >> 4);
+                    const uint64_t v0 = dV + (j % VS) * (kTileBytes >> 4);
 #pragma unroll
                     for (int k = half * 4; k < half * 4 + 4; ++k) {
                         // A = P_t (TMEM, bf16 pairs: 8 columns per 16 kv); B = V [kv][d] MN-major:
                         // 16 kv rows per step (2048 B), d halves LBO = 16 KB apart
-                        mma_ts(tmem + 256 + t * 128, tmem + t * 128 + k * 8, v0 + ((k * 2048) >> 4), idO,
+                        mma_ts(tmem + NT * 128 + t * 128, tmem + t * 128 + k * 8, v0 + ((k * 2048) >> 4), idO,
                                (j | k) != 0);
                     }
                 }
                 __syncwarp();
             };
-            issue_s(0, 0);
-            issue_s(1, 0);
+            for (int t = 0; t < NT; ++t) issue_s(t, 0);
             for (int j = 0; j < nkv; ++j) {
                 const bool more = j + 1 < nkv;
-                for (int t = 0; t < 2; ++t) {
+                for (int t = 0; t < NT; ++t) {
                     wait1(&p_half[t], j & 1);
-                    if (t == 0) wait1(&v_full[j % kVStages], (j / kVStages) & 1);
+                    if (t == 0) wait1(&v_full[j % VS], (j / VS) & 1);
                     if (lane == 0) trace_ev<TR>(j, t, 4);
                     tc_fence_after();
                     issue_pv(t, j, 0);
@@ -377,7 +390,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     issue_pv(t, j, 1);
                     if (leader) {
                         if (!more) mma_commit(&o_final[t]);
-                        if (t == 1) mma_commit(&v_empty[j % kVStages]);
+                        if (t == NT - 1) mma_commit(&v_empty[j % VS]);
                     }
                     __syncwarp();
                     if (more) issue_s(t, j + 1);
@@ -391,7 +404,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const uint32_t q = warp & 3;
         const int row = q * 32 + lane;
         const uint32_t lane_off = (q * 32) << 16;
-        const uint32_t tS = tmem + t * 128 + lane_off, tO = tmem + 256 + t * 128 + lane_off;
+        const uint32_t tS = tmem + t * 128 + lane_off, tO = tmem + NT * 128 + t * 128 + lane_off;
         const float c = a.scale_log2;
         float m_run = -INFINITY, l_run = 0.f;
         for (int j = 0; j < nkv; ++j) {
@@ -416,7 +429,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         // epilogue: O_t / l -> bf16 rows
         mbar_wait(&o_final[t], 0);
         tc_fence_after();
-        const int64_t grow = static_cast<int64_t>(qt) * 2 * kTile + t * kTile + row;
+        const int64_t grow = static_cast<int64_t>(qt) * NT * kTile + t * kTile + row;
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
         if (kAttnOTma) {
             // O_t through Q_t's shared memory (dead: Q_t's last S MMA completed before its
@@ -443,7 +456,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) {
-                const int32_t r0 = static_cast<int32_t>(qt * 2 * kTile + t * kTile + q * 32);
+                const int32_t r0 = static_cast<int32_t>(qt * NT * kTile + t * kTile + q * 32);
                 for (int at = 0; at < 2; ++at)
                     tma_store_3d(&to, stage + at * kAtom + q * 32 * 128, static_cast<int32_t>(h * kHD + at * 64), r0, b);
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -472,7 +485,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 2) tmem_dealloc(tmem, 512);
+    if (warp == 2) tmem_dealloc(tmem, AttnCfg<NT>::tmem_cols);
 }
 
 static int attn_poly() {
@@ -494,6 +507,8 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
         LP_CUDA(cudaFuncSetAttribute(k_attention<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         LP_CUDA(cudaFuncSetAttribute(k_attention<-1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         LP_CUDA(cudaFuncSetAttribute(k_attention<-2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention<6, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     AttnCfg<1>::smem));
         attr = true;
     }
     if ((x.ldq | x.ldk | x.ldv | x.ldo) % 8) fail(LP_ERR_INVALID_ARGUMENT, "attention: strides must be multiples of 8");
@@ -517,6 +532,13 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     const dim3 grid(static_cast<unsigned>((x.n_q + 2 * kTile - 1) / (2 * kTile)), x.heads, x.batch);
     const int cls = x.n_kv == x.n_q && x.q == x.k ? KC_SELF_ATTN : KC_CROSS_ATTN;
     prof_begin(cls, st);
+    // short key sequences (cross-attention over the text tokens): one Q tile per CTA, two CTAs
+    // per SM (AttnCfg<1>)
+    const bool nt1 = x.n_kv <= 4 * kTile && tune_get("attn_nt1", 1) && !tune_get("attn_trace", 0) && attn_poly() == 6;
+    if (nt1) {
+        const dim3 g1(static_cast<unsigned>((x.n_q + kTile - 1) / kTile), x.heads, x.batch);
+        k_attention<6, false, 1><<<g1, AttnCfg<1>::threads, AttnCfg<1>::smem, st>>>(tq, tk, tv, to, a);
+    } else
     switch (tune_get("attn_trace", 0) ? -tune_get("attn_trace", 0) : attn_poly()) {
         case -1: k_attention<0, true><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, to, a); break;
         case -2: k_attention<-1, true><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, to, a); break;

@@ -534,7 +534,9 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     prof_begin(cls, st);
     // short key sequences (cross-attention over the text tokens): one Q tile per CTA, two CTAs
     // per SM (AttnCfg<1>)
-    const bool nt1 = x.n_kv <= 4 * kTile && tune_get("attn_nt1", 1) && !tune_get("attn_trace", 0) && attn_poly() == 6;
+    const int nt1_knob = tune_get("attn_nt1", 1);  // 0 never, 1 short key sequences, 2 always (experiments)
+    const bool nt1 = (nt1_knob == 2 || (nt1_knob == 1 && x.n_kv <= 4 * kTile)) && !tune_get("attn_trace", 0) &&
+                     attn_poly() == 6;
     if (nt1) {
         const dim3 g1(static_cast<unsigned>((x.n_q + kTile - 1) / kTile), x.heads, x.batch);
         k_attention<6, false, 1><<<g1, AttnCfg<1>::threads, AttnCfg<1>::smem, st>>>(tq, tk, tv, to, a);

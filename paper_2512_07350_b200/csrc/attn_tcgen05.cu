@@ -18,6 +18,7 @@
 // S_t(j+1) also certifies that O_t(j) is final before the softmax rescales it.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "dit_ops.hpp"
@@ -63,6 +64,7 @@ struct AttnKernelArgs {
     void* o;
     int64_t ldo;
     float scale_log2;  // softmax scale * log2(e)
+    int heads, batch;
 };
 
 #ifndef LP_ATTN_MAX2
@@ -229,7 +231,7 @@ __device__ __forceinline__ void softmax_block(uint32_t tS, uint32_t tO, int vali
     l_run += ls.x + ls.y;
 }
 
-template <int POLY, bool TR = false, int NT = 2>
+template <int POLY, bool TR = false, int NT = 2, bool PERS = false>
 __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
     k_attention(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                 const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap to, AttnKernelArgs a) {
@@ -249,11 +251,28 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
     uint64_t* p_full = s_full + NT;    // [tile]
     uint64_t* p_half = p_full + NT;    // [tile]
     uint64_t* o_final = p_half + NT;   // [tile]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + NT);
+    uint32_t* tmem_slot;  // after the persistent-mode barriers below
+
+    uint64_t* q_empty = o_final + NT;  // Q smem free (the item's last S MMAs retired)     [persistent]
+    uint64_t* o_empty = q_empty + 1;   // [tile] O_t read out of TMEM by the epilogue     [persistent]
+    uint64_t* epi_done = o_empty + NT; // staging (V slots) read by the epilogue's stores  [persistent]
+    tmem_slot = reinterpret_cast<uint32_t*>(epi_done + 1);
 
     const uint32_t warp = warp_id(), lane = lane_id();
-    const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int nkv = static_cast<int>((a.n_kv + kTile - 1) / kTile);
+    // work items (Q tile group, head, batch).  One per CTA, or a grid-stride walk when the grid
+    // is persistent: item it+1's Q and K stream in while item it drains, its S MMAs queue
+    // behind item it's last PVs, and the epilogue stages O in the (then idle) V slots.
+    const int n_qt = static_cast<int>((a.n_q + NT * kTile - 1) / (NT * kTile));
+    const int items = n_qt * a.heads * a.batch;
+    const int first = PERS ? static_cast<int>(blockIdx.x)
+                           : static_cast<int>(blockIdx.x + n_qt * (blockIdx.y + a.heads * blockIdx.z));
+    const int stride = PERS ? static_cast<int>(gridDim.x) : items;
+    auto item = [&](int w, int& qt, int& h, int& b) {
+        qt = w % n_qt;
+        h = (w / n_qt) % a.heads;
+        b = w / (n_qt * a.heads);
+    };
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tq);
@@ -273,7 +292,10 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
             mbar_init(&p_full[s], 128);
             mbar_init(&p_half[s], 128);
             mbar_init(&o_final[s], 1);
+            mbar_init(&o_empty[s], 128);
         }
+        mbar_init(q_empty, 1);
+        mbar_init(epi_done, 4 * NT);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc(tmem_slot, AttnCfg<NT>::tmem_cols);
@@ -284,46 +306,58 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
 
     if (warp == 0) {
         if (lane == 0) {
-            // K runs ahead in a 3-deep ring (needed first, by S = Q K^T); V in a 2-deep ring
-            const int32_t qrow = static_cast<int32_t>(b * a.q_rows_per_batch + qt * NT * kTile);
-            const int32_t qc = static_cast<int32_t>(a.q_col0 + h * kHD);
-            mbar_arrive_expect_tx(q_full, NT * kTileBytes);
-            for (int t = 0; t < NT; ++t) {
-                tma_load_2d(&tq, q_full, sQ + t * kTileBytes, qc, qrow + t * kTile);
-                tma_load_2d(&tq, q_full, sQ + t * kTileBytes + kAtom, qc + 64, qrow + t * kTile);
-            }
-            const int32_t kc = static_cast<int32_t>(a.k_col0 + h * kHD), vc = static_cast<int32_t>(a.v_col0 + h * kHD);
-            auto load_k = [&](int j) {
-                const int s = j % KS;
-                mbar_wait(&k_empty[s], ((j / KS) & 1) ^ 1);
-                if (POLY == -2 && j >= KS) {  // debug (attn_trace=3): no TMA once the ring is primed
-                    mbar_arrive(&k_full[s]);
-                    return;
+            // K runs ahead in a KS-deep ring (needed first, by S = Q K^T); V in a VS-deep ring.
+            // Ring positions count blocks over all of this CTA's items (g = it * nkv + j).
+            int it = 0;
+            for (int w = first; w < items; w += stride, ++it) {
+                int qt, h, b;
+                item(w, qt, h, b);
+                const int64_t g0 = static_cast<int64_t>(it) * nkv;
+                if (it > 0) mbar_wait(q_empty, (it - 1) & 1);  // the previous item's S MMAs retired
+                const int32_t qrow = static_cast<int32_t>(b * a.q_rows_per_batch + qt * NT * kTile);
+                const int32_t qc = static_cast<int32_t>(a.q_col0 + h * kHD);
+                mbar_arrive_expect_tx(q_full, NT * kTileBytes);
+                for (int t = 0; t < NT; ++t) {
+                    tma_load_2d(&tq, q_full, sQ + t * kTileBytes, qc, qrow + t * kTile);
+                    tma_load_2d(&tq, q_full, sQ + t * kTileBytes + kAtom, qc + 64, qrow + t * kTile);
                 }
-                mbar_arrive_expect_tx(&k_full[s], kTileBytes);
-                const int32_t kr = static_cast<int32_t>(b * a.kv_rows_per_batch + j * kTile);
-                tma_load_2d(&tk, &k_full[s], sK + s * kTileBytes, kc, kr);
-                tma_load_2d(&tk, &k_full[s], sK + s * kTileBytes + kAtom, kc + 64, kr);
-            };
-            auto load_v = [&](int j) {
-                const int s = j % VS;
-                mbar_wait(&v_empty[s], ((j / VS) & 1) ^ 1);
-                if (POLY == -2 && j >= VS) {
-                    mbar_arrive(&v_full[s]);
-                    return;
+                const int32_t kc = static_cast<int32_t>(a.k_col0 + h * kHD), vc = static_cast<int32_t>(a.v_col0 + h * kHD);
+                auto load_k = [&](int j) {
+                    const int64_t g = g0 + j;
+                    const int s = static_cast<int>(g % KS);
+                    mbar_wait(&k_empty[s], static_cast<uint32_t>((g / KS) & 1) ^ 1);
+                    if (POLY == -2 && g >= KS) {  // debug (attn_trace=3): no TMA once the ring is primed
+                        mbar_arrive(&k_full[s]);
+                        return;
+                    }
+                    mbar_arrive_expect_tx(&k_full[s], kTileBytes);
+                    const int32_t kr = static_cast<int32_t>(b * a.kv_rows_per_batch + j * kTile);
+                    tma_load_2d(&tk, &k_full[s], sK + s * kTileBytes, kc, kr);
+                    tma_load_2d(&tk, &k_full[s], sK + s * kTileBytes + kAtom, kc + 64, kr);
+                };
+                auto load_v = [&](int j) {
+                    const int64_t g = g0 + j;
+                    const int s = static_cast<int>(g % VS);
+                    mbar_wait(&v_empty[s], static_cast<uint32_t>((g / VS) & 1) ^ 1);
+                    if (POLY == -2 && g >= VS) {
+                        mbar_arrive(&v_full[s]);
+                        return;
+                    }
+                    mbar_arrive_expect_tx(&v_full[s], kTileBytes);
+                    const int32_t kr = static_cast<int32_t>(b * a.kv_rows_per_batch + j * kTile);
+                    tma_load_2d(&tv, &v_full[s], sV + s * kTileBytes, vc, kr);
+                    tma_load_2d(&tv, &v_full[s], sV + s * kTileBytes + kAtom, vc + 64, kr);
+                };
+                int jk = 0;
+                for (; jk < nkv && jk < KS - 1; ++jk) load_k(jk);
+                for (int j = 0; j < nkv; ++j) {
+                    // single-buffered K (NT = 1): K_j first — S_j needs it before PV_j needs V_j
+                    if (KS == 1 && jk < nkv) load_k(jk++);
+                    // the previous item's epilogue staged O in the V slots
+                    if (j == 0 && it > 0) mbar_wait(epi_done, (it - 1) & 1);
+                    load_v(j);
+                    if (KS > 1 && jk < nkv) load_k(jk++);
                 }
-                mbar_arrive_expect_tx(&v_full[s], kTileBytes);
-                const int32_t kr = static_cast<int32_t>(b * a.kv_rows_per_batch + j * kTile);
-                tma_load_2d(&tv, &v_full[s], sV + s * kTileBytes, vc, kr);
-                tma_load_2d(&tv, &v_full[s], sV + s * kTileBytes + kAtom, vc + 64, kr);
-            };
-            int jk = 0;
-            for (; jk < nkv && jk < KS - 1; ++jk) load_k(jk);
-            for (int j = 0; j < nkv; ++j) {
-                // single-buffered K (NT = 1): K_j first — S_j needs it before PV_j needs V_j
-                if (KS == 1 && jk < nkv) load_k(jk++);
-                load_v(j);
-                if (KS > 1 && jk < nkv) load_k(jk++);
             }
         }
     } else if (warp == 1) {
@@ -337,17 +371,20 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
         // spinning: 32 spinning lanes would steal issue slots from the softmax warps sharing
         // this SMSP
         auto wait1 = [&](uint64_t* bar, uint32_t parity) { mbar_wait_sleep(bar, parity); };
-        {
-            constexpr uint32_t idS = idesc_bf16(128, 128);
-            constexpr uint32_t idO = idesc_bf16(128, 128, /*b_mn_major=*/true);
-            // descriptors built once; per-k offsets go into the start-address field (addr >> 4)
-            const uint64_t dQ = desc_sw128(smem_u32(sQ)), dK = desc_sw128(smem_u32(sK));
-            const uint64_t dV = desc_sw128(smem_u32(sV), /*sbo=*/1024, /*lbo=*/kAtom);
-            wait1(q_full, 0);
+        constexpr uint32_t idS = idesc_bf16(128, 128);
+        constexpr uint32_t idO = idesc_bf16(128, 128, /*b_mn_major=*/true);
+        // descriptors built once; per-k offsets go into the start-address field (addr >> 4)
+        const uint64_t dQ = desc_sw128(smem_u32(sQ)), dK = desc_sw128(smem_u32(sK));
+        const uint64_t dV = desc_sw128(smem_u32(sV), /*sbo=*/1024, /*lbo=*/kAtom);
+        int it = 0;
+        for (int w = first; w < items; w += stride, ++it) {
+            const int64_t g0 = static_cast<int64_t>(it) * nkv;
+            wait1(q_full, it & 1);
             auto issue_s = [&](int t, int j) {
-                const int s = j % KS;
+                const int64_t g = g0 + j;
+                const int s = static_cast<int>(g % KS);
                 if (t == 0) {
-                    wait1(&k_full[s], (j / KS) & 1);
+                    wait1(&k_full[s], static_cast<uint32_t>((g / KS) & 1));
                     tc_fence_after();
                 }
                 if (leader) {
@@ -358,13 +395,16 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
                         mma_ss(tmem + t * 128, q0 + off, k0 + off, idS, k != 0);
                     }
                     mma_commit(&s_full[t]);
-                    if (t == NT - 1) mma_commit(&k_empty[s]);  // every tile's S issued: K_j slot frees on completion
+                    if (t == NT - 1) {
+                        mma_commit(&k_empty[s]);  // every tile's S issued: K_j slot frees on completion
+                        if (j == nkv - 1) mma_commit(q_empty);  // the item's last S: Q smem frees on completion
+                    }
                 }
                 __syncwarp();
             };
             auto issue_pv = [&](int t, int j, int half) {
                 if (leader) {
-                    const uint64_t v0 = dV + (j % VS) * (kTileBytes >> 4);
+                    const uint64_t v0 = dV + ((g0 + j) % VS) * (kTileBytes >> 4);
 #pragma unroll
                     for (int k = half * 4; k < half * 4 + 4; ++k) {
                         // A = P_t (TMEM, bf16 pairs: 8 columns per 16 kv); B = V [kv][d] MN-major:
@@ -378,19 +418,22 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
             for (int t = 0; t < NT; ++t) issue_s(t, 0);
             for (int j = 0; j < nkv; ++j) {
                 const bool more = j + 1 < nkv;
+                const int64_t g = g0 + j;
                 for (int t = 0; t < NT; ++t) {
-                    wait1(&p_half[t], j & 1);
-                    if (t == 0) wait1(&v_full[j % VS], (j / VS) & 1);
+                    wait1(&p_half[t], static_cast<uint32_t>(g & 1));
+                    if (t == 0) wait1(&v_full[g % VS], static_cast<uint32_t>((g / VS) & 1));
+                    // O_t is overwritten by this item's first PV: the previous epilogue read it
+                    if (j == 0 && it > 0) wait1(&o_empty[t], (it - 1) & 1);
                     if (lane == 0) trace_ev<TR>(j, t, 4);
                     tc_fence_after();
                     issue_pv(t, j, 0);
-                    wait1(&p_full[t], j & 1);
+                    wait1(&p_full[t], static_cast<uint32_t>(g & 1));
                     if (lane == 0) trace_ev<TR>(j, t, 5);
                     tc_fence_after();
                     issue_pv(t, j, 1);
                     if (leader) {
                         if (!more) mma_commit(&o_final[t]);
-                        if (t == NT - 1) mma_commit(&v_empty[j % VS]);
+                        if (t == NT - 1) mma_commit(&v_empty[g % VS]);
                     }
                     __syncwarp();
                     if (more) issue_s(t, j + 1);
@@ -406,80 +449,95 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
         const uint32_t lane_off = (q * 32) << 16;
         const uint32_t tS = tmem + t * 128 + lane_off, tO = tmem + NT * 128 + t * 128 + lane_off;
         const float c = a.scale_log2;
-        float m_run = -INFINITY, l_run = 0.f;
-        for (int j = 0; j < nkv; ++j) {
-            mbar_wait(&s_full[t], j & 1);
-            const bool tr0 = TR && (warp & 3) == 2 && lane == 0;
-            if (tr0) trace_ev<TR>(j, t, 0);
+        int it = 0;
+        for (int w = first; w < items; w += stride, ++it) {
+            int qt, h, b;
+            item(w, qt, h, b);
+            const int64_t g0 = static_cast<int64_t>(it) * nkv;
+            float m_run = -INFINITY, l_run = 0.f;
+            for (int j = 0; j < nkv; ++j) {
+                mbar_wait(&s_full[t], static_cast<uint32_t>((g0 + j) & 1));
+                const bool tr0 = TR && (warp & 3) == 2 && lane == 0;
+                if (tr0) trace_ev<TR>(j, t, 0);
+                tc_fence_after();
+                const int valid = static_cast<int>(a.n_kv - static_cast<int64_t>(j) * kTile);
+                // the ragged last key block takes a separately compiled masked copy, so full
+                // blocks carry no per-element compare/select
+                if (POLY < 0) {  // debug (attn_trace=2/3): no softmax work, only the handoffs -> the MMA/sync floor
+                    tc_fence_before();
+                    mbar_arrive(&p_half[t]);
+                    if (tr0) trace_ev<TR>(j, t, 2);
+                    mbar_arrive(&p_full[t]);
+                    if (tr0) trace_ev<TR>(j, t, 3);
+                } else if (valid >= kTile)
+                    softmax_block<POLY, false, TR>(tS, tO, valid, c, m_run, l_run, &p_half[t], &p_full[t], j, t, tr0);
+                else
+                    softmax_block<POLY, true, TR>(tS, tO, valid, c, m_run, l_run, &p_half[t], &p_full[t], j, t, tr0);
+            }
+            // epilogue: O_t / l -> bf16 rows.  The staging below reuses V slots: wait for the
+            // LAST tile's final PV as well (it is the item's last MMA), so no PV still reads V
+            mbar_wait(&o_final[t], it & 1);
+            if (kAttnOTma && t != NT - 1) mbar_wait(&o_final[NT - 1], it & 1);
             tc_fence_after();
-            const int valid = static_cast<int>(a.n_kv - static_cast<int64_t>(j) * kTile);
-            // the ragged last key block takes a separately compiled masked copy, so full
-            // blocks carry no per-element compare/select
-            if (POLY < 0) {  // debug (attn_trace=2/3): no softmax work, only the handoffs -> the MMA/sync floor
-                tc_fence_before();
-                mbar_arrive(&p_half[t]);
-                if (tr0) trace_ev<TR>(j, t, 2);
-                mbar_arrive(&p_full[t]);
-                if (tr0) trace_ev<TR>(j, t, 3);
-            } else if (valid >= kTile)
-                softmax_block<POLY, false, TR>(tS, tO, valid, c, m_run, l_run, &p_half[t], &p_full[t], j, t, tr0);
-            else
-                softmax_block<POLY, true, TR>(tS, tO, valid, c, m_run, l_run, &p_half[t], &p_full[t], j, t, tr0);
-        }
-        // epilogue: O_t / l -> bf16 rows
-        mbar_wait(&o_final[t], 0);
-        tc_fence_after();
-        const int64_t grow = static_cast<int64_t>(qt) * NT * kTile + t * kTile + row;
-        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-        if (kAttnOTma) {
-            // O_t through Q_t's shared memory (dead: Q_t's last S MMA completed before its
-            // last PV, which o_final follows), in the same 128B-swizzled [128 rows x 64 col]
-            // atoms; each warp then TMA-stores its 32 rows as two 64-column boxes.  The 3-D O
-            // map clips rows >= n_q per batch.
-            uint8_t* stage = sQ + t * kTileBytes;
+            const int64_t grow = static_cast<int64_t>(qt) * NT * kTile + t * kTile + row;
+            const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+            if (kAttnOTma) {
+                // O_t staged in V slot t (idle: every PV of the item retired before o_final; the
+                // producer holds the next item's V loads on epi_done) in 128B-swizzled
+                // [128 rows x 64 col] atoms; each warp TMA-stores its 32 rows as two 64-column
+                // boxes.  The 3-D O map clips rows >= n_q per batch.
+                uint8_t* stage = sV + (t % VS) * kTileBytes;
 #pragma unroll 1
-            for (int cc = 0; cc < kHD; cc += 32) {
-                uint32_t r[32];
-                tmem_ld32(tO + cc, r);
-                tmem_ld_wait();
-                uint8_t* arow = stage + (cc >> 6) * kAtom + row * 128;
+                for (int cc = 0; cc < kHD; cc += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(tO + cc, r);
+                    tmem_ld_wait();
+                    uint8_t* arow = stage + (cc >> 6) * kAtom + row * 128;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int unit = ((cc & 63) >> 3) + u;
-                    *reinterpret_cast<uint4*>(arow + ((unit ^ (row & 7)) << 4)) =
-                        make_uint4(pack_bf16(__uint_as_float(r[8 * u + 0]) * inv, __uint_as_float(r[8 * u + 1]) * inv),
-                                   pack_bf16(__uint_as_float(r[8 * u + 2]) * inv, __uint_as_float(r[8 * u + 3]) * inv),
-                                   pack_bf16(__uint_as_float(r[8 * u + 4]) * inv, __uint_as_float(r[8 * u + 5]) * inv),
-                                   pack_bf16(__uint_as_float(r[8 * u + 6]) * inv, __uint_as_float(r[8 * u + 7]) * inv));
-                }
-            }
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-                const int32_t r0 = static_cast<int32_t>(qt * NT * kTile + t * kTile + q * 32);
-                for (int at = 0; at < 2; ++at)
-                    tma_store_3d(&to, stage + at * kAtom + q * 32 * 128, static_cast<int32_t>(h * kHD + at * 64), r0, b);
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                // only the smem READ must finish before the CTA retires (its smem is released);
-                // the global writes complete asynchronously and are visible at grid end
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            }
-            __syncwarp();
-        } else
-#pragma unroll 1
-        for (int cc = 0; cc < kHD; cc += 32) {
-            __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.o) + (b * a.q_rows_per_batch + grow) * a.ldo + h * kHD;
-            uint32_t r[32];
-            tmem_ld32(tO + cc, r);
-            tmem_ld_wait();
-            if (grow < a.n_q) {
-                uint4* o4 = reinterpret_cast<uint4*>(orow + cc);
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    o4[u] = make_uint4(pack_bf16(__uint_as_float(r[8 * u + 0]) * inv, __uint_as_float(r[8 * u + 1]) * inv),
+                    for (int u = 0; u < 4; ++u) {
+                        const int unit = ((cc & 63) >> 3) + u;
+                        *reinterpret_cast<uint4*>(arow + ((unit ^ (row & 7)) << 4)) =
+                            make_uint4(pack_bf16(__uint_as_float(r[8 * u + 0]) * inv, __uint_as_float(r[8 * u + 1]) * inv),
                                        pack_bf16(__uint_as_float(r[8 * u + 2]) * inv, __uint_as_float(r[8 * u + 3]) * inv),
                                        pack_bf16(__uint_as_float(r[8 * u + 4]) * inv, __uint_as_float(r[8 * u + 5]) * inv),
                                        pack_bf16(__uint_as_float(r[8 * u + 6]) * inv, __uint_as_float(r[8 * u + 7]) * inv));
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&o_empty[t]);  // O_t has been read out: the next item's PV may overwrite it
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    const int32_t r0 = static_cast<int32_t>(qt * NT * kTile + t * kTile + q * 32);
+                    for (int at = 0; at < 2; ++at)
+                        tma_store_3d(&to, stage + at * kAtom + q * 32 * 128, static_cast<int32_t>(h * kHD + at * 64), r0, b);
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    // the staging must be read before the V slot is reloaded (or the CTA retires);
+                    // the global writes complete asynchronously and are visible at grid end
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    mbar_arrive(epi_done);
+                }
+                __syncwarp();
+            } else {
+#pragma unroll 1
+                for (int cc = 0; cc < kHD; cc += 32) {
+                    __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.o) + (b * a.q_rows_per_batch + grow) * a.ldo + h * kHD;
+                    uint32_t r[32];
+                    tmem_ld32(tO + cc, r);
+                    tmem_ld_wait();
+                    if (grow < a.n_q) {
+                        uint4* o4 = reinterpret_cast<uint4*>(orow + cc);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            o4[u] = make_uint4(pack_bf16(__uint_as_float(r[8 * u + 0]) * inv, __uint_as_float(r[8 * u + 1]) * inv),
+                                               pack_bf16(__uint_as_float(r[8 * u + 2]) * inv, __uint_as_float(r[8 * u + 3]) * inv),
+                                               pack_bf16(__uint_as_float(r[8 * u + 4]) * inv, __uint_as_float(r[8 * u + 5]) * inv),
+                                               pack_bf16(__uint_as_float(r[8 * u + 6]) * inv, __uint_as_float(r[8 * u + 7]) * inv));
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&o_empty[t]);
+                if (lane == 0) mbar_arrive(epi_done);
             }
         }
     }
@@ -509,6 +567,10 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
         LP_CUDA(cudaFuncSetAttribute(k_attention<-2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
         LP_CUDA(cudaFuncSetAttribute(k_attention<6, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      AttnCfg<1>::smem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention<6, false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     AttnCfg<1>::smem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention<6, false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kAttnSmem));
         attr = true;
     }
     if ((x.ldq | x.ldk | x.ldv | x.ldo) % 8) fail(LP_ERR_INVALID_ARGUMENT, "attention: strides must be multiples of 8");
@@ -529,6 +591,19 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     a.o = x.o;
     a.ldo = x.ldo;
     a.scale_log2 = x.scale * 1.4426950408889634f;
+    a.heads = x.heads;
+    a.batch = x.batch;
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    // persistent grids: CTAs walk the items (knob attn_persist: 0 never, 1 the NT=1 short-key
+    // instance only — cross-attention 640 -> 779 TF/s in-step —, 2 also self-attention, where
+    // it measured slower: 1148-1151 vs 1157-1167 TF/s in-step, profiles/r2b)
+    const int pk = tune_get("attn_persist", 1);
+    const bool ok_p = !tune_get("attn_trace", 0) && attn_poly() == 6;
     const dim3 grid(static_cast<unsigned>((x.n_q + 2 * kTile - 1) / (2 * kTile)), x.heads, x.batch);
     const int cls = x.n_kv == x.n_q && x.q == x.k ? KC_SELF_ATTN : KC_CROSS_ATTN;
     prof_begin(cls, st);
@@ -537,9 +612,17 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     const int nt1_knob = tune_get("attn_nt1", 1);  // 0 never, 1 short key sequences, 2 always (experiments)
     const bool nt1 = (nt1_knob == 2 || (nt1_knob == 1 && x.n_kv <= 4 * kTile)) && !tune_get("attn_trace", 0) &&
                      attn_poly() == 6;
-    if (nt1) {
+    if (nt1 && ok_p && pk >= 1) {
+        const int64_t items = ((x.n_q + kTile - 1) / kTile) * x.heads * x.batch;
+        const unsigned gp = static_cast<unsigned>(std::min<int64_t>(items, 2LL * sms));
+        k_attention<6, false, 1, true><<<gp, AttnCfg<1>::threads, AttnCfg<1>::smem, st>>>(tq, tk, tv, to, a);
+    } else if (nt1) {
         const dim3 g1(static_cast<unsigned>((x.n_q + kTile - 1) / kTile), x.heads, x.batch);
         k_attention<6, false, 1><<<g1, AttnCfg<1>::threads, AttnCfg<1>::smem, st>>>(tq, tk, tv, to, a);
+    } else if (ok_p && pk >= 2) {
+        const int64_t items = ((x.n_q + 2 * kTile - 1) / (2 * kTile)) * x.heads * x.batch;
+        const unsigned gp = static_cast<unsigned>(std::min<int64_t>(items, sms));
+        k_attention<6, false, 2, true><<<gp, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, to, a);
     } else
     switch (tune_get("attn_trace", 0) ? -tune_get("attn_trace", 0) : attn_poly()) {
         case -1: k_attention<0, true><<<grid, kAttnThreads, kAttnSmem, st>>>(tq, tk, tv, to, a); break;

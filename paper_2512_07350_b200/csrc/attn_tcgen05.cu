@@ -269,6 +269,10 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
                            : static_cast<int>(blockIdx.x + n_qt * (blockIdx.y + a.heads * blockIdx.z));
     const int stride = PERS ? static_cast<int>(gridDim.x) : items;
     auto item = [&](int w, int& qt, int& h, int& b) {
+        if (!PERS) {  // one item per CTA: the grid is (Q tile group, head, batch)
+            qt = static_cast<int>(blockIdx.x), h = static_cast<int>(blockIdx.y), b = static_cast<int>(blockIdx.z);
+            return;
+        }
         qt = w % n_qt;
         h = (w / n_qt) % a.heads;
         b = w / (n_qt * a.heads);
@@ -312,7 +316,7 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
             for (int w = first; w < items; w += stride, ++it) {
                 int qt, h, b;
                 item(w, qt, h, b);
-                const int64_t g0 = static_cast<int64_t>(it) * nkv;
+                const uint32_t g0 = PERS ? static_cast<uint32_t>(it) * static_cast<uint32_t>(nkv) : 0u;  // ring position base
                 if (it > 0) mbar_wait(q_empty, (it - 1) & 1);  // the previous item's S MMAs retired
                 const int32_t qrow = static_cast<int32_t>(b * a.q_rows_per_batch + qt * NT * kTile);
                 const int32_t qc = static_cast<int32_t>(a.q_col0 + h * kHD);
@@ -323,9 +327,9 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
                 }
                 const int32_t kc = static_cast<int32_t>(a.k_col0 + h * kHD), vc = static_cast<int32_t>(a.v_col0 + h * kHD);
                 auto load_k = [&](int j) {
-                    const int64_t g = g0 + j;
+                    const uint32_t g = g0 + static_cast<uint32_t>(j);
                     const int s = static_cast<int>(g % KS);
-                    mbar_wait(&k_empty[s], static_cast<uint32_t>((g / KS) & 1) ^ 1);
+                    mbar_wait(&k_empty[s], ((g / KS) & 1u) ^ 1);
                     if (POLY == -2 && g >= KS) {  // debug (attn_trace=3): no TMA once the ring is primed
                         mbar_arrive(&k_full[s]);
                         return;
@@ -336,9 +340,9 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
                     tma_load_2d(&tk, &k_full[s], sK + s * kTileBytes + kAtom, kc + 64, kr);
                 };
                 auto load_v = [&](int j) {
-                    const int64_t g = g0 + j;
+                    const uint32_t g = g0 + static_cast<uint32_t>(j);
                     const int s = static_cast<int>(g % VS);
-                    mbar_wait(&v_empty[s], static_cast<uint32_t>((g / VS) & 1) ^ 1);
+                    mbar_wait(&v_empty[s], ((g / VS) & 1u) ^ 1);
                     if (POLY == -2 && g >= VS) {
                         mbar_arrive(&v_full[s]);
                         return;
@@ -378,13 +382,13 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
         const uint64_t dV = desc_sw128(smem_u32(sV), /*sbo=*/1024, /*lbo=*/kAtom);
         int it = 0;
         for (int w = first; w < items; w += stride, ++it) {
-            const int64_t g0 = static_cast<int64_t>(it) * nkv;
+            const uint32_t g0 = PERS ? static_cast<uint32_t>(it) * static_cast<uint32_t>(nkv) : 0u;  // ring position base
             wait1(q_full, it & 1);
             auto issue_s = [&](int t, int j) {
-                const int64_t g = g0 + j;
+                const uint32_t g = g0 + static_cast<uint32_t>(j);
                 const int s = static_cast<int>(g % KS);
                 if (t == 0) {
-                    wait1(&k_full[s], static_cast<uint32_t>((g / KS) & 1));
+                    wait1(&k_full[s], ((g / KS) & 1u));
                     tc_fence_after();
                 }
                 if (leader) {
@@ -404,7 +408,7 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
             };
             auto issue_pv = [&](int t, int j, int half) {
                 if (leader) {
-                    const uint64_t v0 = dV + ((g0 + j) % VS) * (kTileBytes >> 4);
+                    const uint64_t v0 = dV + ((g0 + static_cast<uint32_t>(j)) % VS) * (kTileBytes >> 4);
 #pragma unroll
                     for (int k = half * 4; k < half * 4 + 4; ++k) {
                         // A = P_t (TMEM, bf16 pairs: 8 columns per 16 kv); B = V [kv][d] MN-major:
@@ -418,16 +422,16 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
             for (int t = 0; t < NT; ++t) issue_s(t, 0);
             for (int j = 0; j < nkv; ++j) {
                 const bool more = j + 1 < nkv;
-                const int64_t g = g0 + j;
+                const uint32_t g = g0 + static_cast<uint32_t>(j);
                 for (int t = 0; t < NT; ++t) {
-                    wait1(&p_half[t], static_cast<uint32_t>(g & 1));
-                    if (t == 0) wait1(&v_full[g % VS], static_cast<uint32_t>((g / VS) & 1));
+                    wait1(&p_half[t], (g & 1u));
+                    if (t == 0) wait1(&v_full[g % VS], ((g / VS) & 1u));
                     // O_t is overwritten by this item's first PV: the previous epilogue read it
                     if (j == 0 && it > 0) wait1(&o_empty[t], (it - 1) & 1);
                     if (lane == 0) trace_ev<TR>(j, t, 4);
                     tc_fence_after();
                     issue_pv(t, j, 0);
-                    wait1(&p_full[t], static_cast<uint32_t>(g & 1));
+                    wait1(&p_full[t], (g & 1u));
                     if (lane == 0) trace_ev<TR>(j, t, 5);
                     tc_fence_after();
                     issue_pv(t, j, 1);
@@ -453,10 +457,10 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
         for (int w = first; w < items; w += stride, ++it) {
             int qt, h, b;
             item(w, qt, h, b);
-            const int64_t g0 = static_cast<int64_t>(it) * nkv;
+            const uint32_t g0 = PERS ? static_cast<uint32_t>(it) * static_cast<uint32_t>(nkv) : 0u;  // ring position base
             float m_run = -INFINITY, l_run = 0.f;
             for (int j = 0; j < nkv; ++j) {
-                mbar_wait(&s_full[t], static_cast<uint32_t>((g0 + j) & 1));
+                mbar_wait(&s_full[t], ((g0 + static_cast<uint32_t>(j)) & 1u));
                 const bool tr0 = TR && (warp & 3) == 2 && lane == 0;
                 if (tr0) trace_ev<TR>(j, t, 0);
                 tc_fence_after();
@@ -477,7 +481,7 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
             // epilogue: O_t / l -> bf16 rows.  The staging below reuses V slots: wait for the
             // LAST tile's final PV as well (it is the item's last MMA), so no PV still reads V
             mbar_wait(&o_final[t], it & 1);
-            if (kAttnOTma && t != NT - 1) mbar_wait(&o_final[NT - 1], it & 1);
+            if (PERS && kAttnOTma && t != NT - 1) mbar_wait(&o_final[NT - 1], it & 1);
             tc_fence_after();
             const int64_t grow = static_cast<int64_t>(qt) * NT * kTile + t * kTile + row;
             const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
@@ -486,7 +490,8 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
                 // producer holds the next item's V loads on epi_done) in 128B-swizzled
                 // [128 rows x 64 col] atoms; each warp TMA-stores its 32 rows as two 64-column
                 // boxes.  The 3-D O map clips rows >= n_q per batch.
-                uint8_t* stage = sV + (t % VS) * kTileBytes;
+                // non-persistent: Q_t's smem is dead (its last S MMA completed before the last PV)
+                uint8_t* stage = PERS ? sV + (t % VS) * kTileBytes : sQ + t * kTileBytes;
 #pragma unroll 1
                 for (int cc = 0; cc < kHD; cc += 32) {
                     uint32_t r[32];

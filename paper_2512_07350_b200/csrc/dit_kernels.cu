@@ -330,6 +330,69 @@ __device__ __forceinline__ uint32_t rdiv(uint32_t x, const RopeDiv& v) {
     return static_cast<uint32_t>((static_cast<uint64_t>(x) * v.mul) >> v.shift);
 }
 
+// RMSNorm over one (row, section) unit of d = 256 * PER8 bf16 held as PER8 16-byte chunks per
+// lane (chunk i of lane l = elements 8 (l + 32 i) .. +7), then the 3-D RoPE from the table;
+// transforms the chunks in place.
+template <int PER8>
+__device__ __forceinline__ void rms_rope_unit(uint4 (&raw)[PER8], uint32_t row, const float* __restrict__ g, float eps,
+                                              const float2* __restrict__ tab, const RopeDivs& dv, int nf, int nh,
+                                              int lane) {
+    constexpr int d = PER8 * 256;
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER8; ++i) {
+        const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[u]));
+            ss += f.x * f.x + f.y * f.y;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+    const float r = rsqrtf(ss / d + eps);
+    const uint32_t tok = row - rdiv(row, dv.batch) * dv.batch.d;
+    const uint32_t tw_ = rdiv(tok, dv.w), pf = rdiv(tw_, dv.h);
+    const int px = static_cast<int>(tok - tw_ * dv.w.d), py = static_cast<int>(tw_ - pf * dv.h.d);
+    // Lane l's 8-element chunks start at 8 (l + 32 i): within a 128-wide head that is pair
+    // 4 (l & 15) for every i, so the lane rotates the same 4 pairs in every head.  Their
+    // (cos, sin) are loaded once per unit, with branch-free table offsets (the per-pair
+    // conditional loads diverged three ways across the warp).
+    float2 cs4[4] = {};
+    if (tab) {
+        const int j0 = 4 * (lane & 15);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u;
+            const int idx = j < 22 ? static_cast<int>(pf) * 22 + j
+                                   : (j < 43 ? nf * 22 + py * 21 + j - 22 : nf * 22 + nh * 21 + px * 21 + j - 43);
+            cs4[u] = tab[idx];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < PER8; ++i) {
+        const int e = 8 * (lane + 32 * i);
+        const float4 ga = reinterpret_cast<const float4*>(g + e)[0], gb = reinterpret_cast<const float4*>(g + e)[1];
+        const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+        const uint32_t in[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
+        uint32_t w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&in[u]));
+            float a = f.x * r * gv[2 * u], b = f.y * r * gv[2 * u + 1];
+            if (tab) {
+                const float2 cs = cs4[u];  // pair ((e & 127) >> 1) + u of the head
+                const float a2 = a * cs.x - b * cs.y, b2 = a * cs.y + b * cs.x;
+                a = a2;
+                b = b2;
+            }
+            const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+            w[u] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        raw[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
 #ifndef LP_RMS_MINB
 #define LP_RMS_MINB 2  // blocks per SM of the persistent grid (ncu A/B: 2 -> 72.0 us, 3 -> 82.2, 4 -> 115.5)
 #endif
@@ -370,48 +433,9 @@ __global__ void __launch_bounds__(256, LP_RMS_MINB) k_rmsnorm_rope_tab(__nv_bflo
 #pragma unroll
             for (int i = 0; i < PER8; ++i) nxt[i] = pn[lane + 32 * i];
         }
-        float ss = 0.f;
+        rms_rope_unit<PER8>(raw, row, g, eps, tab, dv, nf, nh, lane);
 #pragma unroll
-        for (int i = 0; i < PER8; ++i) {
-            const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[u]));
-                ss += f.x * f.x + f.y * f.y;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
-        const float r = rsqrtf(ss / d + eps);
-        const uint32_t tok = row - rdiv(row, dv.batch) * dv.batch.d;
-        const uint32_t tw_ = rdiv(tok, dv.w), pf = rdiv(tw_, dv.h);
-        const int px = static_cast<int>(tok - tw_ * dv.w.d), py = static_cast<int>(tw_ - pf * dv.h.d);
-        const float2* tf = tab + static_cast<int>(pf) * 22;
-        const float2* th = tab + nf * 22 + py * 21 - 22;
-        const float2* tw = tab + nf * 22 + nh * 21 + px * 21 - 43;
-#pragma unroll
-        for (int i = 0; i < PER8; ++i) {
-            const int e = 8 * (lane + 32 * i);
-            const float4 ga = reinterpret_cast<const float4*>(g + e)[0], gb = reinterpret_cast<const float4*>(g + e)[1];
-            const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
-            const uint32_t in[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
-            uint32_t w[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&in[u]));
-                float a = f.x * r * gv[2 * u], b = f.y * r * gv[2 * u + 1];
-                if (tab) {
-                    const int j = ((e & 127) >> 1) + u;  // pair within the head
-                    const float2 cs = j < 22 ? tf[j] : (j < 43 ? th[j] : tw[j]);
-                    const float a2 = a * cs.x - b * cs.y, b2 = a * cs.y + b * cs.x;
-                    a = a2;
-                    b = b2;
-                }
-                const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-                w[u] = *reinterpret_cast<const uint32_t*>(&h);
-            }
-            p[lane + 32 * i] = make_uint4(w[0], w[1], w[2], w[3]);
-        }
+        for (int i = 0; i < PER8; ++i) p[lane + 32 * i] = raw[i];
     }
 }
 

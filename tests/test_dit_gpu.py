@@ -221,3 +221,22 @@ def test_engine_graph_replay_bit_identical_to_eager(cuda):
     assert outs[0][2] == outs[1][2]  # same ledger either way
     # kernel counts differ only by the timestep writes (per forward eagerly, per slot before a replay)
     assert abs(outs[0][1] - outs[1][1]) <= 7 * 4
+
+
+
+@pytest.mark.parametrize("shape", [(16, 5, 16, 16), (16, 3, 9, 19), (16, 9, 60, 104)])
+def test_qk_rope_table_path_matches_per_element_path(cuda, shape):
+    """q/k RMSNorm+RoPE has two independent implementations: the table kernel (per-lane
+    (cos, sin) pairs hoisted per row; the default) and the per-element kernel (knob
+    `rope_tab` 0).  Index errors in either would rotate the wrong pairs and move the DiT
+    output by O(1); the two agree to bf16 rounding (different reduction order)."""
+    z, cond = lp.synthetic_latent(shape, 4, 2025)
+    dit = lp.DiTDenoiser(cond, num_layers=1)
+    outs = []
+    for tab in (0, 1):
+        _lib.check(_lib.lib().lp_tune(b"rope_tab", tab))
+        outs.append(dit.cfg_predict(z, 37, 5.0).data.clone().float())
+        torch.cuda.synchronize()
+    _lib.check(_lib.lib().lp_tune(b"rope_tab", 1))
+    rel = ((outs[0] - outs[1]).norm() / outs[0].norm()).item()
+    assert np.isfinite(rel) and rel <= 5e-3, rel

@@ -201,8 +201,9 @@ uint64_t lp_launch_count(void);
  * 5 K10 reconstruct+update).  collect() fills 6 entries each: launches, device ms,
  * algorithmic FLOPs, algorithmic bytes. */
 int lp_profile_enable(int on);
-/* Kernel-variant knobs (benchmarking): "attn_poly" (0-3: eighths of exp2 on the
- * FMA pipe), "gemm_2sm" (0/1: CTA-pair GEMM).  Also read from LP_TUNE_<KEY>. */
+/* Kernel-variant knobs for A/B measurement (INTEGRATION.md lists all of them with their
+ * defaults), e.g. "attn_poly" (exp2 pairs of every 16 on the FMA pipe: 0, 4, 6, 8),
+ * "gemm_2sm" (0/1: CTA-pair GEMM).  A key's first read also checks LP_TUNE_<KEY>. */
 int lp_tune(const char* key, int value);
 int lp_profile_collect(uint64_t* launches, double* ms, double* flops, double* bytes);
 

@@ -1,20 +1,26 @@
-"""LP denoise benchmark (BASELINE.json metric: LP denoise steps/s, WAN-1.3B-shape
-480p 81f; comm bytes/video).
+"""LP denoise benchmark (BASELINE.json metric: LP denoise steps/s, WAN-1.3B-shape 480p 81f,
+1/2/4/8 B200; comm bytes/video).
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config c2|c4|c5]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
-Workload (BASELINE.json configs[1], "C2"): WAN2.1-1.3B-shaped random-init DiT
-(30 blocks, d=1536, 12 heads, FFN 8960, CFG batch 2) on the 480p/81-frame latent
-16x21x60x104 (f32 storage), patch (1,2,2), LP with K = max(4, N) workers, r = 0.5,
-T = 50-step schedule, eta 0.05, w 5.0, synthetic_inputs seed 2025.  Entries are
-dealt round-robin to the N ranks (N=1 runs all 4 shards on one GPU).  A "step"
-is one LP denoise step: plan, K1 gather, DiT cfg_predict on this rank's shards,
-NCCL all-gather of the eps shards (N>1), K10 blend + sampler update.
+`--gpus N` with N > 1 and no torchrun environment launches N ranks itself (torchrun on
+127.0.0.1, one process per GPU) and fails loudly when fewer than N GPUs are visible; it never
+reports fewer ranks than asked for.  `--plan-only` prints the per-rank shard assignment, the
+exchange bytes and the FLOP-ideal speedup bound for N ranks without touching a GPU.
 
-`value` is device-timed (CUDA events on the engine stream, max over ranks);
-`e2e` is the same steps through the C-ABI engine with the latent copied in from
-pinned host memory and the result copied back every step.
+Workload (BASELINE.json configs[1], "C2", the default): WAN2.1-1.3B-shaped random-init DiT
+(30 blocks, d=1536, 12 heads, FFN 8960, CFG batch 2) on the 480p/81-frame latent 16x21x60x104
+(f32 storage), patch (1,2,2), LP with K = max(4, N) workers, r = 0.5, T = 50-step schedule,
+eta 0.05, w 5.0, synthetic_inputs seed 2025.  Entries are dealt to the N ranks round-robin
+(or balanced by DiT FLOPs, --assign balanced); N=1 runs all 4 shards on one GPU.  A "step" is
+one LP denoise step: plan, K1 gather, DiT cfg_predict on this rank's shards, the ε̂ exchange
+(N>1: NVLink peer stores fused into the DiT epilogue, or NCCL all-gather), K10 blend + sampler
+update.  --config c4 / c5 run BASELINE configs[3] / [4] the same way (K = 8).
+
+`value` is device-timed (CUDA events on the engine stream, max over ranks); `e2e` is the same
+steps through the C-ABI engine with the latent copied in from pinned host memory and the result
+copied back every step.
 """
 from __future__ import annotations
 
@@ -22,7 +28,9 @@ import argparse
 import ctypes as C
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -30,43 +38,134 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-DIMS = (16, 21, 60, 104)
 PATCH = (1, 2, 2)
 T_SCHED = 50
-ETA, W_CFG, SEED, R_OVERLAP = 0.05, 5.0, 2025, 0.5
-METRIC = "LP denoise steps/s, WAN-1.3B-shape 480p 81f (C2)"
+ETA, W_CFG, SEED = 0.05, 5.0, 2025
 UNIT = "steps/s"
 
+# BASELINE.json configs: [1] = C2 (the metric's workload, default), [3] = C4, [4] = C5.
+CONFIGS = {
+    "c2": dict(dims=(16, 21, 60, 104), K=None, schedule=None, dit=dict(), d=1536, F=8960, layers=30, heads=12,
+               metric="LP denoise steps/s, WAN-1.3B-shape 480p 81f (C2)",
+               name="C2: WAN2.1-1.3B-shaped DiT ({L} blocks, d=1536, 12 heads, ffn 8960, CFG batch 2) on 480p81f "
+                    "latent 16x21x60x104 f32"),
+    "c4": dict(dims=(16, 21, 90, 160), K=8, schedule=None, dit=dict(dim=5120, num_heads=40, ffn_dim=13824), d=5120,
+               F=13824, layers=40, heads=40, metric="LP denoise steps/s, WAN-14B-shape 720p 81f (C4)",
+               name="C4: WAN2.1-14B-shaped DiT ({L} blocks, d=5120, 40 heads, ffn 13824, CFG batch 2) on 720p81f "
+                    "latent 16x21x90x160 f32"),
+    "c5": dict(dims=(16, 41, 60, 104), K=8, schedule="TTHTTW", dit=dict(), d=1536, F=8960, layers=30, heads=12,
+               metric="LP denoise steps/s, WAN-1.3B-shape 480p 161f (C5)",
+               name="C5: WAN2.1-1.3B-shaped DiT ({L} blocks, d=1536, 12 heads, ffn 8960, CFG batch 2) on 480p161f "
+                    "latent 16x41x60x104 f32, temporal-heavy schedule TTHTTW"),
+}
 
-# LP_BENCH_GLOO_TEST=1 (torchrun on a ONE-GPU box): every rank on GPU 0, gloo plumbing, no
-# NCCL communicator, ε̂ exchange over CUDA IPC peer memory.  Validates the multi-rank bench
-# path where NCCL refuses two ranks on one device; its numbers are not scaling numbers.
+# LP_BENCH_GLOO_TEST=1 (on a ONE-GPU box): every rank on GPU 0, gloo plumbing, no NCCL
+# communicator, ε̂ exchange over CUDA IPC peer memory.  Validates the multi-rank bench path where
+# NCCL refuses two ranks on one device; its numbers are not scaling numbers.
 GLOO_TEST = os.environ.get("LP_BENCH_GLOO_TEST") == "1"
 
 
-def workload(K, world, layers):
-    return {
-        "workload": f"C2: WAN2.1-1.3B-shaped DiT ({layers} blocks, d=1536, 12 heads, ffn 8960, CFG batch 2) on 480p81f "
-                    f"latent 16x21x60x104 f32, patch (1,2,2), LP K={K} r={R_OVERLAP}, T={T_SCHED}, eta {ETA}, w {W_CFG}",
-        "lp_workers": K, "overlap_ratio": R_OVERLAP, "latent": list(DIMS), "patch": list(PATCH), "schedule_steps": T_SCHED,
-        "ranks": world, "shard_assignment": "round-robin entries over ranks",
-        "l2": "working set > L2 (2.6 GB of bf16 weights streamed per forward, >100 MB activations)",
-    }
+class Cfg:
+    """The run's workload: a BASELINE config, the LP worker count for N ranks, the DiT depth."""
 
+    def __init__(self, args, world):
+        c = CONFIGS[args.config]
+        self.key = args.config
+        self.dims = c["dims"]
+        self.metric = c["metric"]
+        self.r = args.overlap if args.overlap is not None else 0.5
+        self.M = max(1, args.hybrid)
+        self.K = args.workers or c["K"] or (world // self.M if self.M > 1 else max(4, world))
+        self.K1 = args.workers or c["K"] or 4  # the same job's K on one GPU (FLOP-ideal baseline)
+        self.layers = args.layers or c["layers"]
+        self.schedule = c["schedule"]
+        self.d, self.F, self.heads = c["d"], c["F"], c["heads"]
+        self.dit_kwargs = dict(c["dit"], num_layers=self.layers)
+        self.name = c["name"].format(L=self.layers)
+        self.assign = args.assign
 
-def dit_step_flops(plan, layers, d=1536, ffn=8960, text_len=512):
-    """Algorithmic FLOPs of the CFG-batched DiT over every shard of one step's plan
-    (GEMM 2MNK with M = 2n over QKV, O, cross-Q, cross-O, FFN1, FFN2, self-attention 4 n^2 d per batch, cross-attention 4 n 512 d)."""
-    tot = 0.0
-    for k in range(plan.workers):
-        s = plan.sub_shape(DIMS, k)
-        n = -(-s[1] // PATCH[0]) * -(-s[2] // PATCH[1]) * -(-s[3] // PATCH[2])
-        tot += layers * (2 * 2 * n * (6 * d * d + 2 * d * ffn) + 2 * 4 * n * n * d + 2 * 4 * n * text_len * d)
-    return tot
+    def axes(self):
+        from paper_2512_07350_b200 import lp
+
+        return lp.parse_schedule(self.schedule) if self.schedule else [0, 1, 2]
+
+    def axis_of(self, step):
+        a = self.axes()
+        return a[(step - 1) % len(a)]
+
+    def plan(self, step, K=None):
+        from paper_2512_07350_b200 import lp
+
+        a = self.axis_of(step)
+        return lp.build_axis_plan(a, self.dims[1 + a], PATCH[a], step, K or self.K, self.r)
+
+    def tokens(self, shape):
+        return -(-shape[1] // PATCH[0]) * -(-shape[2] // PATCH[1]) * -(-shape[3] // PATCH[2])
+
+    def entry_flops(self, shape):
+        """Algorithmic FLOPs of the CFG-batched DiT on one shard: GEMM 2MNK with M = 2n over QKV, O,
+        cross-Q, cross-O, FFN1, FFN2; self-attention 4 n^2 d per batch; cross-attention 4 n 512 d."""
+        n, d = self.tokens(shape), self.d
+        return self.layers * (2 * 2 * n * (6 * d * d + 2 * d * self.F) + 2 * 4 * n * n * d + 2 * 4 * n * 512 * d)
+
+    def cost_model(self):
+        """lp_shard_layout_ex cost per element (balanced assignment): linear ~ n, attention ~ n^2."""
+        per_tok = self.dims[0] * PATCH[0] * PATCH[1] * PATCH[2]
+        return 4.0 * (6 * self.d ** 2 + 2 * self.d * self.F) / per_tok, 8.0 * self.d / per_tok ** 2
+
+    def layout(self, step, world, K=None):
+        """owner rank of every entry at `step` (the engine's assignment)."""
+        from paper_2512_07350_b200 import lp
+
+        p = self.plan(step, K)
+        lin, quad = self.cost_model()
+        _, _, owner, _ = lp.shard_layout_ex(p, self.dims, world, 0, self.assign, lin, quad)
+        return p, owner
+
+    def workload(self, world):
+        return {
+            "workload": f"{self.name}, patch (1,2,2), LP K={self.K} r={self.r}, T={T_SCHED}, eta {ETA}, w {W_CFG}",
+            "lp_workers": self.K, "overlap_ratio": self.r, "latent": list(self.dims), "patch": list(PATCH),
+            "schedule_steps": T_SCHED, "axis_schedule": self.schedule or "rotating T,H,W", "ranks": world,
+            "shard_assignment": f"{self.assign} entries over ranks",
+            "scaling_note": "strong: one fixed video job; C2 uses K = max(4, N) LP workers, so N = 8 re-partitions "
+                            "the job into 8 shards (the FLOP-ideal bound in scaling_model accounts for it)",
+            "parallelism": f"lp{self.K} over {world} GPU(s)" if self.M == 1 else
+            f"hybrid: {world // self.M} LP groups x {self.M} pipeline stages",
+            "l2": "working set > L2 (2.6 GB of bf16 weights streamed per forward, >100 MB activations)",
+        }
 
 
 def step_index(s):
     return (s - 1) % T_SCHED + 1
+
+
+def scaling_model(cfg, world):
+    """Per-rank DiT FLOPs of the rotation cycle under the engine's assignment, and the FLOP-ideal
+    speedup over the same job on one GPU: mean_axis(total FLOPs at K1) / mean_axis(max-rank FLOPs).
+    It bounds what the N-rank step can reach if every rank ran at the one-GPU throughput."""
+    axes = cfg.axes()
+    per_rank = [[0.0] * world for _ in axes]
+    one_gpu, keff, owners = [], [], []
+    for i in range(len(axes)):
+        p, owner = cfg.layout(i + 1, world)
+        keff.append(p.workers)
+        owners.append(owner)
+        for k in range(p.workers):
+            per_rank[i][owner[k]] += cfg.entry_flops(p.sub_shape(cfg.dims, k))
+        p1 = cfg.plan(i + 1, cfg.K1)
+        one_gpu.append(sum(cfg.entry_flops(p1.sub_shape(cfg.dims, k)) for k in range(p1.workers)))
+    mx = [max(r) for r in per_rank]
+    tot = [sum(r) for r in per_rank]
+    return {
+        "axes": "".join("THW"[a] for a in axes), "k_eff_per_axis": keff,
+        "owner_per_axis": owners,
+        "rank_tflop_per_cycle": [sum(per_rank[i][r] for i in range(len(axes))) / 1e12 for r in range(world)],
+        "max_rank_tflop_per_step_mean": statistics.mean(mx) / 1e12,
+        "one_gpu_tflop_per_step_mean": statistics.mean(one_gpu) / 1e12,
+        "flop_ideal_speedup_vs_1gpu": statistics.mean(one_gpu) / statistics.mean(mx),
+        "rank_balance": statistics.mean(t / world / m for t, m in zip(tot, mx)),
+    }
 
 
 # ---------------------------------------------------------------------------
@@ -122,80 +221,91 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the reference's own run_lp (oracle/_ref = unmodified lpsim) at C2
+# The reference's CPU path: the UNMODIFIED reference run_lp (oracle/_ref) with a CPU DiT
 # ---------------------------------------------------------------------------
-def cpu_reference_run(steps, K, threads):
-    import numpy as np
-
+def cpu_reference_run(cfg, steps, threads):
+    """LP machinery alone: the reference run_lp with its own box denoiser (rho=1) at the shape."""
     from oracle.oracle import Oracle, Reference, reference_available
 
     os.environ["LPSIM_THREADS"] = str(threads)
     kind = "reference" if reference_available() else "port"
     lib = Reference() if kind == "reference" else Oracle()
-    z, cond = lib.synthetic(DIMS, 4, SEED)
+    z, cond = lib.synthetic(cfg.dims, 4, SEED)
     t0 = time.perf_counter()
-    lib.run_lp(0, (1, 1, 1), z, 4, steps, ETA, W_CFG, cond, PATCH, K, R_OVERLAP)
+    lib.run_lp(0, (1, 1, 1), z, 4, steps, ETA, W_CFG, cond, PATCH, cfg.K, cfg.r)
     dt = time.perf_counter() - t0
-    used = min(threads, K) if kind == "reference" else 1
-    sample = (f"reference run_lp (box denoiser rho=1 in place of the DiT: the reference has none), C2 latent "
-              f"16x21x60x104 f32, K={K}, r={R_OVERLAP}, {steps} steps; LPSIM_THREADS={threads} "
+    used = min(threads, cfg.K) if kind == "reference" else 1
+    sample = (f"reference run_lp (box denoiser rho=1 in place of the DiT: the reference has none), latent "
+              f"{'x'.join(map(str, cfg.dims))} f32, K={cfg.K}, r={cfg.r}, {steps} steps; LPSIM_THREADS={threads} "
               f"(the pool uses min(threads, K) workers; extract/reconstruct/sampler are single-threaded)")
-    del np
     return steps / dt, {"kind": kind, "cores": used, "sample": sample, "seconds": dt}
 
 
-def reference_dit_step(ref, dit, z, cond, K, flop_scale):
-    """One bounded sample of the reference arm: the UNMODIFIED reference run_lp (oracle/_ref)
-    for one step with the fp32 CPU DiT (one block) in its Denoiser slot; the DiT's wall time
-    is scaled to the full 30 blocks and to the rotation-cycle mean shard FLOPs."""
-    import time as _t
-
-    dit.calls.clear()
-    t0 = _t.perf_counter()
-    ref.run_lp_callback(dit.predict, z, 4, 1, ETA, W_CFG, cond, PATCH, K, R_OVERLAP)
-    wall = _t.perf_counter() - t0
-    dit_wall = max(e for _, e in dit.calls) - min(s for s, _ in dit.calls)
-    return (wall - dit_wall) + dit_wall * flop_scale, wall, dit_wall
-
-
-def reference_dit_baseline(K, threads, samples, warmup):
-    """The reference's CPU path on the metric's workload: the UNMODIFIED reference run_lp
-    (oracle/_ref) with the fp32 CPU WAN-1.3B DiT in its Denoiser slot (oracle/cpu_dit.py),
-    `samples` bounded samples (see reference_dit_step).  Returns (steps/s, sample text)."""
+def _cpu_dit(cfg, layers):
     import torch
 
-    from oracle.cpu_dit import CpuDiT, dit_flops
-    from oracle.oracle import Reference, sub_shape
+    from oracle.cpu_dit import CpuDiT
 
-    os.environ["LPSIM_THREADS"] = str(threads)
-    workers = min(threads, K)
-    torch.set_num_threads(max(1, threads // workers))
+    kw = dict(cfg.dit_kwargs)
+    kw.pop("num_layers", None)
+    return CpuDiT(num_layers=layers, dtype=torch.bfloat16, **kw)
+
+
+def reference_full_steps(cfg, steps, threads):
+    """The reference arm's measurement: the UNMODIFIED reference run_lp (oracle/_ref) for `steps`
+    whole LP steps (step 1 = T axis, then H, W ...) with the full-depth bf16 CPU DiT in its
+    Denoiser slot (oracle/cpu_dit.py).  Nothing is scaled: the wall time is what ran."""
+    import torch
+
+    from oracle.oracle import Reference
+
+    os.environ["LPSIM_THREADS"] = "0"  # serial workers: each predict() gets every host thread
+    torch.set_num_threads(threads)
     ref = Reference()
-    z, cond = ref.synthetic(DIMS, 4, SEED)
-    dit = CpuDiT(num_layers=1)
+    z, cond = ref.synthetic(cfg.dims, 4, SEED)
+    dit = _cpu_dit(cfg, cfg.layers)
+    # warm-up outside the timing: page in oneDNN's AMX kernels on a small shard, one block's shape
+    dit.predict(z[:, :1, :8, :8], 1, cond, True)
+    dit.calls.clear()
+    t0 = time.perf_counter()
+    _, _, trace = ref.run_lp_callback(dit.predict, z, 4, steps, ETA, W_CFG, cond, PATCH, cfg.K, cfg.r, trace=True)
+    wall = time.perf_counter() - t0
+    dit_s = sum(e - s for s, e in dit.calls)
+    return wall, dit_s, len(dit.calls)
 
-    def axis_flops(step):  # the reference's own plans
-        p = ref.build_plan(DIMS, PATCH, step, K, R_OVERLAP)
-        return sum(dit_flops(sub_shape(DIMS, p, k), PATCH) for k in range(p.n))
 
-    cycle = sum(axis_flops(s) for s in (1, 2, 3)) / 3
-    scale = 30 * cycle / axis_flops(1)   # run_lp's single sampled step is step 1 (T axis)
-    for _ in range(warmup):
-        reference_dit_step(ref, dit, z, cond, K, scale)
-    est, walls, dits = [], [], []
-    for _ in range(samples):
-        e, w, dw = reference_dit_step(ref, dit, z, cond, K, scale)
-        est.append(e)
-        walls.append(w)
-        dits.append(dw)
-    value = len(est) / sum(est)
-    sample = (f"UNMODIFIED reference run_lp (oracle/_ref) for 1 step (T axis) of C2 (16x21x60x104 f32, K={K}, "
-              f"r={R_OVERLAP}, eta {ETA}, w {W_CFG}) with an fp32 torch CPU WAN-1.3B-shaped DiT (1 of 30 blocks, "
-              f"random weights) in its Denoiser slot; {samples} sample(s): measured wall {statistics.mean(walls):.2f} s "
-              f"of which DiT {statistics.mean(dits):.2f} s, DiT part scaled x{scale:.2f} (30 blocks x cycle-mean/T-axis "
-              f"shard FLOPs); LPSIM_THREADS={threads}, {workers} workers x {torch.get_num_threads()} torch threads; "
-              f"{warmup} warm-up sample(s)")
-    return value, sample
+def reference_sample(cfg, threads):
+    """Bounded sample for our arm's cpu_baseline (about 10-30 s of CPU work): the reference run_lp
+    for one step (T axis) with a ONE-block bf16 CPU DiT in its Denoiser slot; the DiT's share is
+    scaled to the full depth (all blocks have one shape) and to the cycle-mean shard FLOPs."""
+    import torch
+
+    from oracle.oracle import Reference
+
+    os.environ["LPSIM_THREADS"] = "0"
+    torch.set_num_threads(threads)
+    ref = Reference()
+    z, cond = ref.synthetic(cfg.dims, 4, SEED)
+    dit = _cpu_dit(cfg, 1)
+    dit.predict(z[:, :1, :8, :8], 1, cond, True)
+    dit.calls.clear()
+    t0 = time.perf_counter()
+    ref.run_lp_callback(dit.predict, z, 4, 1, ETA, W_CFG, cond, PATCH, cfg.K, cfg.r)
+    wall = time.perf_counter() - t0
+    dit_s = sum(e - s for s, e in dit.calls)
+
+    def axis_flops(step):
+        p = cfg.plan(step)
+        return sum(cfg.entry_flops(p.sub_shape(cfg.dims, k)) for k in range(p.workers))
+
+    cyc = statistics.mean(axis_flops(i + 1) for i in range(len(cfg.axes())))
+    scale = cfg.layers * cyc / axis_flops(1)
+    est = (wall - dit_s) + dit_s * scale
+    sample = (f"UNMODIFIED reference run_lp (oracle/_ref), 1 step (T axis) of {cfg.key.upper()} with a ONE-block "
+              f"bf16 CPU DiT (oracle/cpu_dit.py, AMX) in its Denoiser slot: wall {wall:.2f} s of which DiT {dit_s:.2f} s; "
+              f"DiT share scaled x{scale:.2f} ({cfg.layers} blocks x cycle-mean/T-axis shard FLOPs); serial workers, "
+              f"{threads} torch threads.  bench.py --impl reference times whole {cfg.layers}-block steps instead")
+    return 1.0 / est, sample
 
 
 def run_reference_arm(args, rank, world):
@@ -203,26 +313,67 @@ def run_reference_arm(args, rank, world):
         return
     from oracle.oracle import reference_available
 
-    K = args.workers or max(4, world)
-    threads = os.cpu_count() or 1
+    cfg = Cfg(args, world)
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     if not reference_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (the compiled reference) was not built"}))
         return
-    # LP machinery alone (reference run_lp with its box denoiser, rho=1): what the reference runs without a DiT
-    cpu_reference_run(1, K, threads)
-    lp_only, lp_info = cpu_reference_run(args.steps, K, threads)
-    # the metric's workload: reference run_lp + a WAN-1.3B-shaped fp32 DiT in the Denoiser slot
-    value, sample = reference_dit_baseline(K, threads, args.steps, min(args.warmup, 1))
+    cpu_reference_run(cfg, 1, threads)
+    lp_only, lp_info = cpu_reference_run(cfg, 20, threads)
+    # whole steps of the metric's workload: one rotation cycle (T, H, W), nothing extrapolated
+    n = args.ref_steps or len(cfg.axes())
+    wall, dit_s, calls = reference_full_steps(cfg, n, threads)
+    value = n / wall
+    sample = (f"UNMODIFIED reference run_lp (oracle/_ref) for {n} whole LP steps (steps 1..{n}: axes "
+              f"{''.join('THW'[cfg.axis_of(i)] for i in range(1, n + 1))}) of {cfg.key.upper()} "
+              f"({'x'.join(map(str, cfg.dims))} f32, K={cfg.K}, r={cfg.r}, eta {ETA}, w {W_CFG}) with the full "
+              f"{cfg.layers}-block WAN-shaped DiT (bf16 GEMM/attention on AMX, fp32 residual; random weights) in its "
+              f"Denoiser slot, {calls} predict() calls; wall {wall:.1f} s of which DiT {dit_s:.1f} s; serial workers "
+              f"(LPSIM_THREADS=0), {threads} torch threads.  Timed once: the requested --steps {args.steps} "
+              f"--warmup {args.warmup} would take {(args.steps + args.warmup) * wall / n / 60:.0f} min")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64 (LP machinery) / f32 (CPU DiT)", "data": "synthetic (synthetic_inputs seed 2025)",
-        "config": workload(K, world, 30),
+        "impl": "reference", "metric": cfg.metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": n,
+        "warmup": 0, "ms_per_step": 1000.0 * wall / n, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16 (CPU DiT GEMM/attention) / f64 (LP machinery)",
+        "data": "synthetic (synthetic_inputs seed 2025; random-init weights)",
+        "config": cfg.workload(world),
+        "requested": {"steps": args.steps, "warmup": args.warmup},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "lp_machinery_only": {"value": lp_only, "unit": UNIT, "cores": lp_info["cores"], "sample": lp_info["sample"]},
     }
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# plan only (no GPU): the assignment, exchange bytes and FLOP-ideal bound for N ranks
+# ---------------------------------------------------------------------------
+def run_plan_only(args, rank, world):
+    import torch.distributed as dist
+
+    from paper_2512_07350_b200 import lp
+
+    cfg = Cfg(args, world)
+    mine = {"rank": rank, "owned_entries": {}, "tokens": {}}
+    for a in sorted(set(cfg.axes())):
+        p, owner = cfg.layout(cfg.axes().index(a) + 1, world)
+        ks = [k for k in range(p.workers) if owner[k] == rank]
+        mine["owned_entries"]["THW"[a]] = [k + 1 for k in ks]
+        mine["tokens"]["THW"[a]] = [cfg.tokens(p.sub_shape(cfg.dims, k)) for k in ks]
+    ranks = [mine]
+    if world > 1:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, mine)
+    if rank != 0:
+        return
+    ag = led = 0
+    for i in range(1, T_SCHED + 1):
+        a, b = lp.step_comm_bytes(cfg.plan(i), cfg.dims, 2, world // cfg.M, 4)
+        led += a
+        ag += b
+    print(json.dumps({"mode": "plan-only", "metric": cfg.metric, "n_gpus": world, "config": cfg.workload(world),
+                      "ranks": ranks, "scaling_model": scaling_model(cfg, world),
+                      "comm": {"allgather_bytes_per_video": ag, "reference_ledger_bytes_per_video": led}}), flush=True)
 
 
 # ---------------------------------------------------------------------------
@@ -237,22 +388,23 @@ def run_ours(args, rank, world, local_rank):
     L = _lib.lib()
     torch.cuda.set_device(local_rank)
     _lib.check(L.lp_device_check(local_rank))
-    M = max(1, args.hybrid)
+    cfg = Cfg(args, world)
+    M = cfg.M
     if world % M:
         raise SystemExit(f"--hybrid {M} must divide the number of GPUs {world}")
-    K = args.workers or (world // M if M > 1 else max(4, world))
-    z_host_np, cond = lp.synthetic_latent_host(DIMS, 4, SEED)
-    dit = lp.DiTDenoiser(cond, num_layers=args.layers)
+    dims, K = cfg.dims, cfg.K
+    z_host_np, cond = lp.synthetic_latent_host(dims, 4, SEED)
+    dit = lp.DiTDenoiser(cond, **cfg.dit_kwargs)
     nccl_id = None
-    if world > 1 and not GLOO_TEST:
+    if world > 1 and not GLOO_TEST and (args.exchange == "nccl" or M > 1):
         obj = [lp.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    eng = lp.LpEngine(DIMS, PATCH, 4, K, R_OVERLAP, T_SCHED, ETA, W_CFG, cond, denoiser="dit", dit=dit, world=world,
-                      rank=rank, nccl_id=nccl_id, group_size=M)
-    exchange = "nccl" if world > 1 else "none"
+    eng = lp.LpEngine(dims, PATCH, 4, K, cfg.r, T_SCHED, ETA, W_CFG, cond, denoiser="dit", dit=dit, world=world,
+                      rank=rank, nccl_id=nccl_id, group_size=M, schedule=cfg.schedule, assign=cfg.assign)
+    exchange = "nccl" if nccl_id is not None else "none"
     if world > 1 and M == 1 and args.exchange == "peer":
-        # K9 over NVLink peer memory (CUDA IPC); every rank must map every peer, else all stay on NCCL
+        # K9 over NVLink peer memory (CUDA IPC); every rank must map every peer, else fall back to NCCL
         handles = [None] * world
         dist.all_gather_object(handles, eng.ipc_handle())
         ok = 1
@@ -265,11 +417,21 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         if int(t.item()) == 1:
             exchange = "peer"
-        elif ok:
-            eng.ipc_detach()
+        else:
+            if ok:
+                eng.ipc_detach()
+            if GLOO_TEST:
+                raise SystemExit("peer attach failed under LP_BENCH_GLOO_TEST (no NCCL fallback on one GPU)")
+            eng.close()
+            obj = [lp.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            eng = lp.LpEngine(dims, PATCH, 4, K, cfg.r, T_SCHED, ETA, W_CFG, cond, denoiser="dit", dit=dit,
+                              world=world, rank=rank, nccl_id=obj[0], schedule=cfg.schedule, assign=cfg.assign)
+            exchange = "nccl"
     z0 = torch.from_numpy(z_host_np.astype("float32")).pin_memory()
     eng.z.data.copy_(z0)
     stream = torch.cuda.current_stream()
+    tmo = args.sync_timeout
 
     def barrier():
         if world > 1:
@@ -282,10 +444,10 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # warm-up
+    # warm-up (every axis's graph is captured on its second occurrence)
     for s in range(1, args.warmup + 1):
         eng.run(step_index(s), 1)
-    torch.cuda.synchronize()
+    eng.sync(tmo)
 
     # ---- device-timed region: K steps, inputs resident in HBM ----
     first = args.warmup + 1
@@ -298,16 +460,15 @@ def run_ours(args, rank, world, local_rank):
         for s in range(first, first + args.steps):
             eng.run(step_index(s), 1)
         ev1.record(stream)
-        torch.cuda.synchronize()
+        eng.sync(tmo)  # a dead or stalled peer raises WorkerFailure instead of hanging
     barrier()
     launches = int(L.lp_launch_count() - l0)
-    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    my_ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(my_ms)
     c1 = eng.comm()
-    nl = (C.c_uint64 * 6)()
-    kms, kfl, kby = (C.c_double * 6)(), (C.c_double * 6)(), (C.c_double * 6)()
 
     # ---- end-to-end through the C-ABI engine with host buffers ----
-    zin = torch.empty(DIMS, dtype=torch.float32).pin_memory()
+    zin = torch.empty(dims, dtype=torch.float32).pin_memory()
     zin.copy_(z0)
     zout = torch.empty_like(zin).pin_memory()
     barrier()
@@ -319,7 +480,7 @@ def run_ours(args, rank, world, local_rank):
         eng.run(step_index(s), 1)
         zout.copy_(eng.z.data, non_blocking=True)         # D2H: the step's result
     e1.record(stream)
-    torch.cuda.synchronize()
+    eng.sync(tmo)
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
     assert torch.isfinite(zout).all(), "non-finite latent"
@@ -336,53 +497,75 @@ def run_ours(args, rank, world, local_rank):
         if int(lo.item()) != int(hi.item()):
             raise SystemExit(f"rank {rank}: replicated latent differs across ranks after the run")
 
-    # ---- per-kernel roofline pass: one rotation cycle (T, H, W) with the shard streams
-    # serialised, so each kernel's CUDA-event duration is its own (in the timed region two
-    # shards' DiT forwards overlap on two streams and per-kernel durations would overlap) ----
+    # ---- K9 alone: back-to-back exchanges of the first timed step's full slots (NVLink GB/s) ----
+    xbench = None
+    if world > 1 and M == 1:
+        barrier()
+        xms, xbytes = eng.exchange_bench(step_index(first), args.exchange_iters)
+        xbench = {"iters": args.exchange_iters, "ms": xms, "bytes_received": xbytes,
+                  "GBps": xbytes / xms / 1e6 if xms else None}
+
+    # ---- per-kernel roofline pass: one rotation cycle with the shard streams serialised, so
+    # each kernel's CUDA-event duration is its own (in the timed region two shards' DiT
+    # forwards overlap on two streams and per-kernel durations would overlap) ----
+    nl = (C.c_uint64 * 6)()
+    kms, kfl, kby = (C.c_double * 6)(), (C.c_double * 6)(), (C.c_double * 6)()
+    ncyc = len(cfg.axes())
+    barrier()
     L.lp_tune(b"engine_serial", 1)
     L.lp_profile_enable(1)
     pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     pe0.record(stream)
-    for s in range(first, first + 3):
+    for s in range(first, first + ncyc):
         eng.run(step_index(s), 1)
     pe1.record(stream)
-    torch.cuda.synchronize()
+    eng.sync(tmo)
     L.lp_profile_enable(0)
     L.lp_tune(b"engine_serial", 0)
     prof_ms = pe0.elapsed_time(pe1)
     _lib.check(L.lp_profile_collect(nl, kms, kfl, kby))
 
+    # ---- per-rank report ----
+    owned = {}
+    for a in sorted(set(cfg.axes())):
+        p, owner = cfg.layout(cfg.axes().index(a) + 1, world)
+        owned["THW"[a]] = [k + 1 for k in range(p.workers) if owner[k] == rank]
+    mine = {"rank": rank, "owned_entries": owned, "ms_timed": my_ms, "exchange": exchange,
+            "bytes_received_timed": (c1["nccl_bytes_received"] - c0["nccl_bytes_received"]),
+            "exchange_bench": xbench, "launches_timed": launches,
+            "exchange_in_step": {"ms": kms[3], "launches": int(nl[3]), "bytes": kby[3],
+                                 "note": "push+flag+wait inside the serialised profiling cycle: includes peer skew"}}
+    ranks = [mine]
+    if world > 1:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, mine)
     if rank != 0:
         eng.close()
         return
     names = ["self_attention", "cross_attention", "gemm"]
     kern = {names[i]: {"launches": int(nl[i]), "ms": kms[i], "tflops": (kfl[i] / kms[i] / 1e9) if kms[i] else None,
                        "share_of_step": kms[i] / prof_ms if prof_ms else None} for i in range(3)}
-    peaks_hbm = None
+    peaks = {}
     try:
-        peaks_hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    peaks_hbm = peaks_hbm or 7700.0
+    peaks_hbm = peaks.get("hbm_gbs") or 7700.0
     hbm = {}
     for i, nm in ((4, "k1_gather"), (5, "k10_reconstruct_update")):
         gbps = kby[i] / kms[i] / 1e6 if kms[i] else None
         hbm[nm] = {"launches": int(nl[i]), "ms": kms[i], "algorithmic_bytes": kby[i], "GBps": gbps,
                    "frac_of_hbm": gbps / peaks_hbm if gbps else None, "share_of_step": kms[i] / prof_ms if prof_ms else None}
     hbm["peak_GBps"] = peaks_hbm
-    hbm["peak_source"] = "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"
+    hbm["peak_source"] = "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)" if peaks.get("hbm_gbs") else "fallback 7700"
     ag = None
-    if world > 1:
-        ag_gbps = kby[3] / kms[3] / 1e6 if kms[3] else None
-        ag = {"launches": int(nl[3]), "ms": kms[3], "bytes_received_per_rank": kby[3], "GBps_per_rank": ag_gbps,
-              "nvlink_peak_GBps_per_direction": 900.0, "frac": ag_gbps / 900.0 if ag_gbps else None,
-              "share_of_step": kms[3] / prof_ms if prof_ms else None}
+    if world > 1 and xbench:
+        ag = {"exchange": exchange, "bench_GBps_per_rank": [r["exchange_bench"]["GBps"] for r in ranks],
+              "nvlink_peak_GBps_per_direction": 900.0,
+              "frac": min(r["exchange_bench"]["GBps"] for r in ranks) / 900.0,
+              "bytes_received_per_rank_per_step": ranks[0]["exchange_bench"]["bytes_received"] / args.exchange_iters,
+              "in_step_launches": int(nl[3])}
     dom = max(range(3), key=lambda i: kms[i])
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
     peak = peaks.get("bf16_tflops_sustained") or 1400.0
     achieved = kfl[dom] / kms[dom] / 1e9 if kms[dom] else None
     traffic = None
@@ -391,67 +574,98 @@ def run_ours(args, rank, world, local_rank):
         traffic = prof.get(names[dom], {}).get("dram_bytes_per_launch")
     except Exception:
         pass
-    # whole-step algorithmic FLOPs (DiT on every shard of the rotation cycle, CFG batch 2)
-    step_flops = statistics.mean(dit_step_flops(lp.build_plan(DIMS, PATCH, s, K, R_OVERLAP), args.layers)
-                                 for s in (1, 2, 3)) / world
+    sm = scaling_model(cfg, world)
+    # whole-step algorithmic FLOPs per rank (the max-loaded rank sets the step), CFG batch 2
+    step_flops = sm["max_rank_tflop_per_step_mean"] * 1e12
     step_tflops = step_flops / (ms / args.steps / 1000.0) / 1e12
-    # communication per video (50 steps): measured NCCL bytes, exact all-gather layout, reference ledger, NMP
-    per_step_nccl = (c1["nccl_bytes_received"] - c0["nccl_bytes_received"]) * world / args.steps
+    # communication per video (50 steps): measured exchange bytes, exact all-gather layout, reference ledger, NMP
+    per_step_x = sum(r["bytes_received_timed"] for r in ranks) / args.steps
     led = ag_video = 0
     for i in range(1, T_SCHED + 1):
-        p = lp.build_plan(DIMS, PATCH, i, K, R_OVERLAP)
-        a, b = lp.step_comm_bytes(p, DIMS, 2, world // M, 4)
+        a, b = lp.step_comm_bytes(cfg.plan(i), dims, 2, world // M, 4)
         led += a
         ag_video += b
-    tokens = (DIMS[1] // PATCH[0]) * (DIMS[2] // PATCH[1]) * (DIMS[3] // PATCH[2])
-    nmp = 2 * T_SCHED * (K - 1) * tokens * 1536 * 2
+    tokens = cfg.tokens(dims)
+    nmp = 2 * T_SCHED * (K - 1) * tokens * cfg.d * 2
     value = args.steps / (ms / 1000.0)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "metric": cfg.metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (synthetic_inputs seed 2025; random-init weights, pinned generator)",
-        "config": workload(K, world, args.layers),
+        "config": cfg.workload(world),
         "e2e": {"value": args.steps / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": zin.numel() * 4,
                 "d2h_bytes_per_step": zout.numel() * 4},
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "kernel": names[dom], "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if achieved else None, "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)",
-                     "timing": "CUDA events around every launch on its stream, over one rotation cycle (3 steps) "
+                     "timing": "CUDA events around every launch on its stream, over one schedule cycle "
                                "run right after the timed region with the shard streams serialised",
-                     "step": {"algorithmic_tflop_per_step_per_rank": step_flops / 1e12, "achieved": step_tflops,
+                     "step": {"algorithmic_tflop_per_step_max_rank": step_flops / 1e12, "achieved": step_tflops,
                               "frac": step_tflops / peak}},
         "kernels": kern,
         "hbm_kernels": hbm,
         "allgather": ag,
         "clocks": clk.summary(),
         "exchange": exchange,
-        "comm": {"nccl_bytes_per_step_measured_all_ranks": per_step_nccl,
+        "ranks": ranks,
+        "scaling_model": sm,
+        "comm": {"exchange_bytes_per_step_measured_all_ranks": per_step_x,
                  "allgather_bytes_per_video": ag_video, "reference_ledger_bytes_per_video": led,
                  "reference_nmp_bytes_per_video": nmp, "wire": "f32 eps shards (ledger counts the 2-B preset width)"},
     }
     if M > 1:
         hy = eng.hybrid()
-        cr = lp.cost_report(T_SCHED, world, R_OVERLAP, DIMS, PATCH, preset="custom", hidden_dim=dit.cfg.dim,
+        cr = lp.cost_report(T_SCHED, world, cfg.r, dims, PATCH, preset="custom", hidden_dim=dit.cfg.dim,
                             wire_bytes=4, hybrid=(world // M, [M] * (world // M)))
-        line["config"]["parallelism"] = f"hybrid: {world // M} LP groups x {M} pipeline stages"
         line["hybrid"] = {"group_size": M, "groups": world // M, "rank0_layers": [hy["layer_begin"], hy["layer_end"]],
                           "reference_cost_hybrid_intra_bytes_per_video_fp32": cr["hybrid"]["C_intra_total"],
                           "reference_cost_hybrid_bound": cr["hybrid"]["bound"]}
     if world == 1 and not args.no_cpu_baseline:
         from oracle.oracle import reference_available
 
-        threads = os.cpu_count() or 1
-        v_lp, info = cpu_reference_run(args.cpu_steps, K, threads)
+        threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+        v_lp, info = cpu_reference_run(cfg, args.cpu_steps, threads)
         line["cpu_baseline_lp_machinery_only"] = {"value": v_lp, "unit": UNIT, "cores": info["cores"],
                                                   "kind": info["kind"], "sample": info["sample"]}
         if reference_available():
-            v, sample = reference_dit_baseline(K, threads, 1, 0)
+            v, sample = reference_sample(cfg, threads)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample}
         else:
             line["cpu_baseline"] = dict(line["cpu_baseline_lp_machinery_only"])
     print(json.dumps(line), flush=True)
     eng.close()
+
+
+# ---------------------------------------------------------------------------
+# launch
+# ---------------------------------------------------------------------------
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(args):
+    """--gpus N without a torchrun environment: start N ranks with torchrun ourselves (one
+    process per GPU, rendezvous on 127.0.0.1).  Fails loudly when N GPUs are not visible."""
+    n = args.gpus
+    if not args.plan_only and not GLOO_TEST and not (args.impl == "reference"):
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < n:
+            raise SystemExit(f"bench.py --gpus {n}: only {have} CUDA device(s) visible; refusing to report fewer ranks")
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # the communicator's nranks shows in the log
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    r = subprocess.run(cmd, env=env)
+    if r.returncode:
+        raise SystemExit(f"bench.py --gpus {n}: a rank failed (torchrun exit {r.returncode})")
 
 
 def main():
@@ -460,36 +674,49 @@ def main():
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workers", type=int, default=0, help="LP workers K (default max(4, N))")
-    ap.add_argument("--layers", type=int, default=30)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS), help="BASELINE config (default c2 = configs[1])")
+    ap.add_argument("--workers", type=int, default=0, help="LP workers K (default max(4, N); C4/C5: 8)")
+    ap.add_argument("--layers", type=int, default=0, help="DiT blocks (default: the config's)")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="N > 1: eps exchange over NVLink peer memory fused into the DiT epilogue (default), or NCCL")
+    ap.add_argument("--assign", default="round-robin", choices=["round-robin", "balanced"],
+                    help="entry -> rank assignment (balanced: longest-processing-time on DiT FLOPs)")
     ap.add_argument("--hybrid", type=int, default=1,
                     help="M > 1: hybrid LP x model parallelism, N/M LP groups of M pipeline stages (K = N/M)")
     ap.add_argument("--overlap", type=float, default=None,
                     help="LP overlap ratio r (BASELINE configs[2] sweep; default 0.5 = configs[1])")
     ap.add_argument("--cpu-steps", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-steps", type=int, default=0, help="reference arm: whole LP steps to time (default: one cycle)")
+    ap.add_argument("--exchange-iters", type=int, default=20)
+    ap.add_argument("--sync-timeout", type=float, default=600.0, help="seconds before a stalled step is a WorkerFailure")
+    ap.add_argument("--plan-only", action="store_true", help="print the N-rank assignment and FLOP-ideal bound (no GPU)")
     args = ap.parse_args()
-    if args.overlap is not None:
-        global R_OVERLAP
-        R_OVERLAP = args.overlap
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        self_launch(args)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} launched with WORLD_SIZE={world}")
     local_rank = 0 if GLOO_TEST else int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
     if world > 1:
-        import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        if GLOO_TEST:  # validation of the multi-rank bench on ONE GPU: gloo plumbing, peer exchange
+        if args.plan_only or GLOO_TEST:  # CPU plumbing / validation of the multi-rank bench on ONE GPU
             dist.init_process_group("gloo")
         else:
+            import torch
+
+            torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    run_ours(args, rank, world, local_rank)
+    if args.plan_only:
+        run_plan_only(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
 

@@ -124,12 +124,22 @@ int lp_plan_offsets(const lp_plan* plan, const int64_t shape[4], int64_t* offset
  * (entry e -> rank e % world).  For `rank`, writes the entry ids it owns
  * (owned_out, up to LP_MAX_WORKERS) and their count; slot_elems_out = the
  * padded per-rank slot of the all-gather buffer (max over ranks of the summed
- * elements it owns).  Rank r's slot holds its entries packed in worker order. */
+ * elements it owns, rounded up to a multiple of 8 elements so every slot starts
+ * 16-byte aligned).  Rank r's slot holds its entries packed in worker order. */
 int lp_shard_layout(const lp_plan* plan, const int64_t shape[4], int world, int rank, int32_t* owned_out,
                     int32_t* n_owned_out, int64_t* slot_elems_out);
 /* Element offset of every entry's ε̂ shard inside the gathered buffer
  * (world slots of slot_elems): the layout K10 reads after the all-gather. */
 int lp_shard_bases(const lp_plan* plan, const int64_t shape[4], int world, int64_t* base_out);
+/* The same layout under an assignment policy: LP_ASSIGN_ROUND_ROBIN, or LP_ASSIGN_BALANCED =
+ * longest-processing-time greedy on cost(entry) = lin*elems + quad*elems^2 (ties -> lowest
+ * rank; with K <= world it equals round-robin).  The reference leaves the worker -> device
+ * mapping open (its workers are threads, src/cluster.cpp:115-162).  owner_out / base_out:
+ * one value per entry (NULL to skip). */
+enum lp_assign { LP_ASSIGN_ROUND_ROBIN = 0, LP_ASSIGN_BALANCED = 1 };
+int lp_shard_layout_ex(const lp_plan* plan, const int64_t shape[4], int world, int rank, int32_t policy, double lin,
+                       double quad, int32_t* owned_out, int32_t* n_owned_out, int64_t* slot_elems_out,
+                       int32_t* owner_out, int64_t* base_out);
 
 /* Communication accounting — CommLedger + run_lp metering (src/cluster.cpp:27-73,
  * 186-209): the reference ledger bytes of step i (2 passes x (scatter+gather)
@@ -360,6 +370,9 @@ typedef struct lp_engine_config {
      * activation to the next stage (ncclSend/Recv).  Entries are assigned to groups.  0 or 1
      * = plain LP.  Requires the DiT denoiser. */
     int32_t group_size;
+    /* Entry -> rank assignment (lp_assign).  LP_ASSIGN_BALANCED weighs entries by the
+     * DiT's FLOPs (linear layers ~ tokens, self-attention ~ tokens^2), toys by elements. */
+    int32_t assign;
 } lp_engine_config;
 
 typedef struct lp_engine lp_engine;
@@ -404,6 +417,20 @@ int lp_engine_owned(const lp_engine* e, int32_t step, int32_t* n_owned);
 /* Group decomposition of this rank and the activation bytes it handed to the next stage. */
 int lp_engine_hybrid(const lp_engine* e, int32_t* group_size, int32_t* group, int32_t* stage, int32_t* layer_begin,
                      int32_t* layer_end, uint64_t* intra_bytes);
+/* Waits for everything enqueued on `stream` (the host side of run_workers' join,
+ * src/cluster.cpp:149-161), polling instead of blocking: an NCCL asynchronous error
+ * (ncclCommGetAsyncError) or `timeout_ms` (> 0) without completion aborts the
+ * communicator and returns LP_ERR_WORKER_FAILURE naming the step; a peer whose ε̂ shard
+ * never arrived over the NVLink exchange returns LP_ERR_WORKER_FAILURE naming the lowest
+ * worker id that rank owns ("worker k failed at step i: rank r ..."), and K10 has left z
+ * at the previous step instead of blending stale shards. */
+int lp_engine_sync(lp_engine* e, void* stream, int64_t timeout_ms);
+/* K9 alone, for its NVLink roofline: `iters` back-to-back exchanges of step's full ε̂ slots
+ * (peer: the unfused remote-store push + flag + wait; NCCL: the all-gather), timed with CUDA
+ * events on `stream`.  Every rank must call it with the same arguments.  bytes_out = bytes
+ * this rank received (slot x (world-1) x iters). */
+int lp_engine_exchange_bench(lp_engine* e, int32_t step, int32_t iters, void* stream, double* ms_out,
+                             uint64_t* bytes_out);
 /* Bytes this engine moved over NCCL so far, and the reference ledger bytes. */
 int lp_engine_comm(const lp_engine* e, uint64_t* nccl_bytes, uint64_t* ledger_bytes);
 /* Kernel launches issued by the engine so far (this library's kernels only). */

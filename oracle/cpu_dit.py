@@ -8,10 +8,13 @@ into the reference's own `run_lp` through its Denoiser interface (oracle/ref_har
 `ref_run_lp_callback`).  Weights are random (torch.Generator, fixed seed): the arm
 measures time, not values.
 
-Bounded sample: a full C2 step is ~630 TFLOP (hours on host cores), so one sample is
-one reference `run_lp` step with a ONE-block DiT; the DiT wall time of that step is
-scaled by the block count (all blocks have identical shapes and cost) and by the ratio
-of the rotation-cycle mean DiT FLOPs to the sampled axis's FLOPs.
+Precision: `dtype=torch.bfloat16` (the arm's default) runs every GEMM and attention in bf16
+with fp32 accumulation on the host's AMX tiles (oneDNN), residual stream and norms in fp32 —
+the GPU arm's arithmetic, and ~2.5x faster on the box's 16 Sapphire-Rapids-class cores than
+fp32 (probe: 11 vs 2.6 TF/s GEMM, 5 vs 2.3 TF/s SDPA; profiles/r3a).  A full C2 LP step is
+~630 TFLOP, so bench.py --impl reference times whole reference run_lp steps (a T/H/W cycle)
+with all 30 blocks; bench.py's in-line cpu_baseline uses a bounded one-block sample scaled to
+the metric's unit instead (see bench.py).
 """
 from __future__ import annotations
 
@@ -49,7 +52,7 @@ class CpuDiT:
     """fp32 CPU DiT with the engine's architecture; predict() is one CFG pass
     (the reference's Denoiser::predict: uncond when the conditioning is null)."""
 
-    def __init__(self, num_layers=1, seed=2025, **overrides):
+    def __init__(self, num_layers=1, seed=2025, dtype=torch.float32, **overrides):
         c = dict(WAN13B, **overrides)
         c["num_layers"] = num_layers
         self.cfg = SimpleNamespace(**c)
@@ -75,17 +78,75 @@ class CpuDiT:
                 self.ck.append(rms(ctx @ p[pre + "ck.w"].t() + p[pre + "ck.b"], p[pre + "cnorm_k"], self.cfg.eps))
                 self.cv.append(ctx @ p[pre + "cv.w"].t() + p[pre + "cv.b"])
         del d
+        self.dtype = dtype
+        self.p = params
+        if dtype != torch.float32:  # GEMM / attention operands in `dtype`, fp32 residual and norms
+            self.w = {k: v.to(dtype) for k, v in params.items() if v.dim() == 2}
+            self.ck = [k.to(dtype) for k in self.ck]
+            self.cv = [v.to(dtype) for v in self.cv]
         self._lock = threading.Lock()
         self.calls = []  # (start, end) perf_counter of every predict call
 
     def predict(self, z, t, cond, is_null):
         t0 = time.perf_counter()
-        out = self.ref.predict(torch.from_numpy(np.asarray(z, np.float32)), int(t), self.ck, self.cv, 0 if is_null else 1)
+        zt = torch.from_numpy(np.asarray(z, np.float32))
+        if self.dtype == torch.float32:
+            out = self.ref.predict(zt, int(t), self.ck, self.cv, 0 if is_null else 1)
+        else:
+            out = self._predict_lowp(zt, int(t), 0 if is_null else 1)
         res = out.double().numpy()
         t1 = time.perf_counter()
         with self._lock:
             self.calls.append((t0, t1))
         return res
+
+    @torch.no_grad()
+    def _predict_lowp(self, z, t, b):
+        """One CFG pass with bf16 GEMM / attention operands (fp32 accumulate), fp32 elsewhere:
+        the forward of oracle/dit_fp32.DiTReference.run at the GPU arm's precision."""
+        from oracle.dit_fp32 import apply_rope, rope_tables, sinusoid
+
+        c, p, W, lp_ = self.cfg, self.p, self.w, self.dtype
+        d, L, heads, eps = c.dim, c.num_layers, c.num_heads, c.eps
+
+        def lin(x, name):
+            return (x.to(lp_) @ W[name + ".w"].t()).float() + p[name + ".b"]
+
+        def att(q, k, v):
+            n = q.shape[0]
+            q, k, v = (a.to(lp_).view(a.shape[0], heads, -1).transpose(0, 1)[None] for a in (q, k, v))
+            return torch.nn.functional.scaled_dot_product_attention(q, k, v)[0].transpose(0, 1).reshape(n, d)
+
+        pt, ph, pw = c.patch
+        C, F, H, Wd = z.shape
+        nf, nh, nw = -(-F // pt), -(-H // ph), -(-Wd // pw)
+        zp = torch.zeros(C, nf * pt, nh * ph, nw * pw)
+        zp[:, :F, :H, :Wd] = z
+        x = lin(zp.view(C, nf, pt, nh, ph, nw, pw).permute(1, 3, 5, 0, 2, 4, 6).reshape(nf * nh * nw, -1), "patch")
+        s = sinusoid(c.freq_dim, t * c.t_scale)
+        silu = torch.nn.functional.silu
+        e = silu(s[None] @ p["time.w1"].t() + p["time.b1"]) @ p["time.w2"].t() + p["time.b2"]
+        e0 = (silu(e) @ p["time.wp"].t() + p["time.bp"]).view(6, d)
+        mods = p["blocks.mod"].view(L, 6, d) + e0[None]
+        cos, sin = rope_tables(nf, nh, nw, "cpu")
+        ln = torch.nn.functional.layer_norm
+        for l in range(L):
+            pre, m = f"blocks.{l}.", mods[l]
+            h = ln(x, (d,), eps=eps) * (1 + m[1]) + m[0]
+            qkv = lin(h, pre + "qkv")
+            q = apply_rope(rms(qkv[:, :d], p[pre + "norm_q"], eps), cos, sin, heads)
+            k = apply_rope(rms(qkv[:, d:2 * d], p[pre + "norm_k"], eps), cos, sin, heads)
+            x = x + lin(att(q, k, qkv[:, 2 * d:]), pre + "o") * m[2]
+            h = ln(x, (d,), weight=p[pre + "norm3.w"], bias=p[pre + "norm3.b"], eps=eps)
+            cq = rms(lin(h, pre + "cq"), p[pre + "cnorm_q"], eps)
+            x = x + lin(att(cq, self.ck[l][b], self.cv[l][b]), pre + "co")
+            h = ln(x, (d,), eps=eps) * (1 + m[4]) + m[3]
+            f = torch.nn.functional.gelu(lin(h, pre + "ffn1"), approximate="tanh")
+            x = x + lin(f, pre + "ffn2") * m[5]
+        hm = p["head.mod"].view(2, d) + e
+        head = lin(ln(x, (d,), eps=eps) * (1 + hm[1]) + hm[0], "head")
+        out = head.view(nf, nh, nw, pt, ph, pw, C).permute(6, 0, 3, 1, 4, 2, 5).reshape(C, nf * pt, nh * ph, nw * pw)
+        return out[:, :F, :H, :Wd]
 
 
 def dit_flops(shape, patch, dim=1536, ffn=8960, text_len=512):

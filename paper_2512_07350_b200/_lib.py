@@ -57,7 +57,8 @@ class EngineConfig(C.Structure):
                 ("mode", C.c_int32), ("eta", C.c_double), ("guidance", C.c_double), ("denoiser", C.c_int32),
                 ("wire_bytes", C.c_int32), ("radius", C.c_int64 * 3), ("t_coeff", C.c_double),
                 ("cond_coeff", C.c_double), ("world", C.c_int32), ("rank", C.c_int32), ("dit", C.c_void_p),
-                ("schedule_len", C.c_int32), ("schedule", C.c_int32 * 64), ("group_size", C.c_int32)]
+                ("schedule_len", C.c_int32), ("schedule", C.c_int32 * 64), ("group_size", C.c_int32),
+                ("assign", C.c_int32)]
 
 
 class CostReport(C.Structure):
@@ -91,6 +92,8 @@ _SIGS = {
     "lp_plan_offsets": (_i, [_PlanP, _i64p, _i64p]),
     "lp_shard_layout": (_i, [_PlanP, _i64p, _i, _i, C.POINTER(_i32), C.POINTER(_i32), _i64p]),
     "lp_shard_bases": (_i, [_PlanP, _i64p, _i, _i64p]),
+    "lp_shard_layout_ex": (_i, [_PlanP, _i64p, _i, _i, _i32, _d, _d, C.POINTER(_i32), C.POINTER(_i32), _i64p,
+                                C.POINTER(_i32), _i64p]),
     "lp_step_comm_bytes":(_i, [_PlanP, _i64p, _i, _i, _i, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "lp_cost_report": (_i, [_i, _i, _d, _i64p, _i64p, _i64, _i, _i, C.POINTER(_i32), C.POINTER(CostReport)]),
     "lp_f16_encode": (C.c_uint16, [_d]),
@@ -151,6 +154,8 @@ _SIGS = {
     "lp_engine_destroy": (_i, [_vp]),
     "lp_engine_latent": (_i, [_vp, C.POINTER(_vp)]),
     "lp_engine_run": (_i, [_vp, _i32, _i32, _vp]),
+    "lp_engine_sync": (_i, [_vp, _vp, _i64]),
+    "lp_engine_exchange_bench": (_i, [_vp, _i32, _i32, _vp, _f64p, C.POINTER(C.c_uint64)]),
     "lp_engine_comm": (_i, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "lp_engine_launches": (_i, [_vp, C.POINTER(C.c_uint64)]),
 }

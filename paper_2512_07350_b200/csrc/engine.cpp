@@ -15,7 +15,10 @@
 // runs all K workers' shards on one GPU ("K ranks on one GPU").
 #include <nccl.h>
 
+#include <chrono>
 #include <cstring>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "recon.hpp"
@@ -54,16 +57,19 @@ struct lp_engine {
     // exchange over CUDA-IPC peer memory (lp_engine_ipc_attach): arena = 2 gather buffers
     // (epoch parity) + per-rank flag words + the push kernel's arrival counter
     uint8_t* arena = nullptr;
-    size_t gather_bytes = 0, flags_off = 0;
+    // status block: {missing-peer mask, step} at +0, the device exchange epoch at +64
+    size_t gather_bytes = 0, flags_off = 0, status_off = 0;
     bool peer = false;
     uint8_t* peer_arena[kMaxPeers + 1] = {};
     unsigned long long epoch = 0;
     uint64_t peer_bytes = 0;
+    int last_step = 0;  // last step issued (failure attribution)
     // DiT engines replay each axis's step as a CUDA graph (captured the second time the
     // axis comes up, so every kernel's one-time setup has run eagerly first)
-    cudaGraphExec_t graph[3] = {};
-    uint64_t graph_kernels[3] = {};
-    int seen[3] = {};
+    // (peer-exchange engines: one graph per (axis, gather-buffer parity))
+    cudaGraphExec_t graph[6] = {};
+    uint64_t graph_kernels[6] = {};
+    int seen[6] = {};
     cudaStream_t cap_stream = nullptr;  // capture happens here (the caller's stream may be the legacy default)
 };
 
@@ -119,11 +125,24 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
             e->cond_mean = acc / static_cast<double>(n_cond);
         }
         try {
+            if (c->assign != LP_ASSIGN_ROUND_ROBIN && c->assign != LP_ASSIGN_BALANCED)
+                fail(LP_ERR_INVALID_ARGUMENT, "assign must be 0 (round-robin) or 1 (balanced)");
+            AssignCost cost;  // toys: elements
+            if (c->dit) {
+                // DiT FLOPs per entry with n = elems / (C * patch volume) tokens, CFG batch 2:
+                // linear 4 n (6 d^2 + 2 d F) + self-attention 8 n^2 d
+                lp_dit_config dc;
+                lp_dit_get_config(c->dit, &dc);
+                const double per_tok = static_cast<double>(e->shape.c) * dc.patch[0] * dc.patch[1] * dc.patch[2];
+                cost.lin = 4.0 * (6.0 * dc.dim * dc.dim + 2.0 * dc.dim * dc.ffn_dim) / per_tok;
+                cost.quad = 8.0 * dc.dim / (per_tok * per_tok);
+            }
             i64 max_slot = 0;
             for (int a = 0; a < 3; ++a) {
                 // step index a+1 has axis a; step_index is cosmetic in the plan
                 e->plans[a] = build_plan_for_shape(e->shape, c->patch, a + 1, c->workers, c->overlap_ratio);
-                e->layout[a] = shard_layout(e->plans[a], e->shape, e->groups, e->M > 1 ? e->group : c->rank);
+                e->layout[a] = shard_layout(e->plans[a], e->shape, e->groups, e->M > 1 ? e->group : c->rank,
+                                            c->assign == LP_ASSIGN_BALANCED ? &cost : nullptr);
                 e->elems[a] = entry_elems(e->plans[a], e->shape);
                 e->recon[a] = make_recon_params(e->plans[a], e->shape, e->layout[a].base, c->eta);
                 max_slot = std::max(max_slot, e->layout[a].slot_elems);
@@ -132,7 +151,8 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
             LP_CUDA(cudaMalloc(&e->z, static_cast<size_t>(e->shape.volume()) * E));
             e->gather_bytes = (static_cast<size_t>(max_slot) * e->groups * E + 255) / 256 * 256;
             e->flags_off = 2 * e->gather_bytes;
-            const size_t arena = e->flags_off + (static_cast<size_t>(c->world) * 8 + 8 + 255) / 256 * 256;
+            e->status_off = e->flags_off + (static_cast<size_t>(c->world) * 8 + 8 + 255) / 256 * 256;
+            const size_t arena = e->status_off + 256;
             LP_CUDA(cudaMalloc(&e->arena, arena));
             LP_CUDA(cudaMemset(e->arena, 0, arena));
             e->gather = e->arena;
@@ -155,13 +175,19 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
             }
             LP_CUDA(cudaMalloc(&e->ws, lp_toy_workspace_bytes(c->shape) + 64));
             if (c->dit) {
-                // workspace for the largest shard the DiT will see (tokens per entry)
+                // workspace for the largest shard the DiT will see: tokens per entry with the DiT's
+                // own patch and ceil division (remainder rows pad a partial patch), the count
+                // lp_dit_cfg_predict_slot / lp_dit_forward_layers compute
+                lp_dit_config dc;
+                lp_dit_get_config(c->dit, &dc);
                 i64 max_tokens = 0;
                 for (int a = 0; a < 3; ++a)
                     for (int k = 0; k < e->plans[a].n_entries; ++k) {
                         const Shape4 s = e->shape.with_extent(a, e->plans[a].entries[k].latent_end -
                                                                      e->plans[a].entries[k].latent_begin);
-                        max_tokens = std::max(max_tokens, (s.t / c->patch[0]) * (s.h / c->patch[1]) * (s.w / c->patch[2]));
+                        const i64 nt = (s.t + dc.patch[0] - 1) / dc.patch[0], nh = (s.h + dc.patch[1] - 1) / dc.patch[1],
+                                  nw = (s.w + dc.patch[2] - 1) / dc.patch[2];
+                        max_tokens = std::max(max_tokens, nt * nh * nw);
                     }
                 const int st = lp_dit_reserve_slots(c->dit, max_tokens, e->nslots);
                 if (st) fail(st, lp_last_error());
@@ -213,6 +239,17 @@ int lp_engine_latent(lp_engine* e, void** z) {
 }  // extern "C"
 
 namespace {
+
+// Captured step graphs bake the exchange mode (peer stores, gather-buffer parity): drop them
+// whenever the mode changes.
+void reset_graphs(lp_engine* e) {
+    for (int g = 0; g < 6; ++g) {
+        if (e->graph[g]) cudaGraphExecDestroy(e->graph[g]);
+        e->graph[g] = nullptr;
+        e->graph_kernels[g] = 0;
+        e->seen[g] = 0;
+    }
+}
 
 int step_axis(const lp_engine* e, int i) {
     const lp_engine_config& c = e->cfg;
@@ -371,10 +408,11 @@ void step_exchange_peer(lp_engine* e, int i, cudaStream_t st, bool fused) {
     }
     pp.off = slot * static_cast<size_t>(c.rank);
     pp.bytes = fused ? 0 : slot;  // fused: the slot already went out with the DiT epilogue; signal only
-    pp.epoch = e->epoch;
+    pp.epoch = reinterpret_cast<unsigned long long*>(e->arena + e->status_off + 64);
     prof_begin(KC_ALLGATHER, st);
     peer_push(pp, reinterpret_cast<unsigned*>(e->arena + e->flags_off + static_cast<size_t>(c.world) * 8), st);
-    peer_wait(reinterpret_cast<const unsigned long long*>(e->arena + e->flags_off), c.world, c.rank, e->epoch, st);
+    peer_wait(reinterpret_cast<const unsigned long long*>(e->arena + e->flags_off), c.world, c.rank, pp.epoch,
+              reinterpret_cast<unsigned*>(e->arena + e->status_off), i, st);
     prof_end(KC_ALLGATHER, st, 0.0, static_cast<double>(slot) * (c.world - 1));
     e->peer_bytes += static_cast<uint64_t>(slot) * (c.world - 1);
 }
@@ -410,7 +448,9 @@ void run_step_graph(lp_engine* e, int i, cudaStream_t st) {
     const lp_engine_config& c = e->cfg;
     const int a = step_axis(e, i);
     const int t = c.total_steps + 1 - i;
-    if (++e->seen[a] < 2 && !e->graph[a]) {
+    const int par = e->peer ? static_cast<int>((e->epoch + 1) & 1) : 0;  // the parity this step will use
+    const int g_ix = 2 * a + par;
+    if (++e->seen[g_ix] < 2 && !e->graph[g_ix]) {
         run_step_eager(e, i, st);
         return;
     }
@@ -418,7 +458,7 @@ void run_step_graph(lp_engine* e, int i, cudaStream_t st) {
         const int rc = lp_dit_set_time(c.dit, s, t, st);
         if (rc) fail(rc, lp_last_error());
     }
-    if (!e->graph[a]) {
+    if (!e->graph[g_ix]) {
         lp_dit_time_on_device(c.dit, 1);
         const uint64_t l0 = launch_count();
         cudaGraph_t g = nullptr;
@@ -435,14 +475,19 @@ void run_step_graph(lp_engine* e, int i, cudaStream_t st) {
         }
         LP_CUDA(cudaStreamEndCapture(cs, &g));
         lp_dit_time_on_device(c.dit, 0);
-        e->graph_kernels[a] = launch_count() - l0;
-        const cudaError_t err = cudaGraphInstantiate(&e->graph[a], g, 0);
+        e->graph_kernels[g_ix] = launch_count() - l0;
+        const cudaError_t err = cudaGraphInstantiate(&e->graph[g_ix], g, 0);
         cudaGraphDestroy(g);
         LP_CUDA(err);
     } else {
-        count_launch(e->graph_kernels[a]);  // the replay runs the captured kernels again
+        count_launch(e->graph_kernels[g_ix]);  // the replay runs the captured kernels again
+        if (e->peer) {  // the host side of run_step_eager / step_exchange_peer for the replayed step
+            ++e->epoch;
+            e->gather = e->arena + static_cast<size_t>(e->epoch & 1) * e->gather_bytes;
+            e->peer_bytes += static_cast<uint64_t>(e->layout[a].slot_elems) * c.dtype_bytes * (c.world - 1);
+        }
     }
-    LP_CUDA(cudaGraphLaunch(e->graph[a], st));
+    LP_CUDA(cudaGraphLaunch(e->graph[g_ix], st));
 }
 
 }  // namespace
@@ -459,11 +504,13 @@ int lp_engine_run(lp_engine* e, int32_t first, int32_t count, void* stream) {
         const uint64_t l0 = launch_count();
         // graphs: DiT engines, on a stream that can be captured, unless per-launch profiling
         // or the serialised debug mode is on (both need the eager launches)
-        // (multi-rank engines stay eager: their step holds an ncclAllGather, and a capture
-        // failure there would cost a scaling run for no device-time gain — DESIGN.md §6)
-        const bool graphs = e->cfg.dit != nullptr && e->comm == nullptr && !e->peer && tune_get("engine_graph", 1) &&
-                            !prof_enabled() && !tune_get("engine_serial", 0);
+        // (NCCL-exchange engines stay eager: their step holds an ncclAllGather; the peer
+        // exchange is plain kernels on device memory, so its steps are captured too, one graph
+        // per (axis, gather-buffer parity), with the exchange epoch kept on the device)
+        const bool graphs = e->cfg.dit != nullptr && (e->peer || e->comm == nullptr) && e->M == 1 &&
+                            tune_get("engine_graph", 1) && !prof_enabled() && !tune_get("engine_serial", 0);
         for (int i = first; i < first + count; ++i) {
+            e->last_step = i;
             if (graphs) run_step_graph(e, i, st);
             else run_step_eager(e, i, st);
             account_step(e, i);
@@ -560,7 +607,9 @@ int lp_engine_ipc_attach(lp_engine* e, const uint8_t* handles) {
             LP_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
             e->peer_arena[j] = static_cast<uint8_t*>(p);
         }
+        reset_graphs(e);
         e->peer = true;  // takes precedence over an NCCL communicator for the ε̂ exchange
+        for (auto& r : e->recon) r.abort = reinterpret_cast<const unsigned*>(e->arena + e->status_off);
     });
 }
 
@@ -571,8 +620,107 @@ int lp_engine_ipc_detach(lp_engine* e) {
                 LP_CUDA(cudaIpcCloseMemHandle(p));
                 p = nullptr;
             }
+        reset_graphs(e);
         e->peer = false;
         e->gather = e->arena;
+        for (auto& r : e->recon) r.abort = nullptr;
+    });
+}
+
+// Failure attribution in the reference's terms: "worker k failed at step i: ..." with k the
+// lowest failing worker id (src/cluster.cpp:149-161); a dead rank fails every entry it owns.
+static std::string failed_workers(const lp_engine* e, unsigned rank_mask, int step) {
+    const int a = step >= 1 && step <= e->cfg.total_steps ? step_axis(e, step) : 0;
+    const ShardLayout& L = e->layout[a];
+    int worst = -1, rank = -1;
+    for (size_t k = 0; k < L.owner.size(); ++k)
+        if ((rank_mask >> L.owner[k]) & 1u) {
+            worst = static_cast<int>(k) + 1;
+            rank = L.owner[k];
+            break;
+        }
+    if (worst < 0) {  // the rank owned no entry at this step
+        for (int r = 0; r < 32; ++r)
+            if ((rank_mask >> r) & 1u) { rank = r; break; }
+        return "rank " + std::to_string(rank) + " failed at step " + std::to_string(step);
+    }
+    return "worker " + std::to_string(worst) + " failed at step " + std::to_string(step) + ": rank " +
+           std::to_string(rank);
+}
+
+int lp_engine_sync(lp_engine* e, void* stream, int64_t timeout_ms) {
+    return guard([&] {
+        cudaStream_t st = as_stream(stream);
+        const auto t0 = std::chrono::steady_clock::now();
+        for (;;) {
+            const cudaError_t q = cudaStreamQuery(st);
+            if (q == cudaSuccess) break;
+            if (q != cudaErrorNotReady) fail(LP_ERR_CUDA, std::string("step ") + std::to_string(e->last_step) + ": " + cudaGetErrorString(q));
+            if (e->comm) {
+                ncclResult_t r = ncclSuccess;
+                ncclCommGetAsyncError(e->comm, &r);
+                if (r != ncclSuccess && r != ncclInProgress) {
+                    const std::string why = ncclGetErrorString(r);
+                    ncclCommAbort(e->comm);
+                    e->comm = nullptr;
+                    fail(LP_ERR_WORKER_FAILURE, "step " + std::to_string(e->last_step) + ": NCCL exchange failed: " + why);
+                }
+            }
+            const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+            if (timeout_ms > 0 && ms > timeout_ms) {
+                if (e->comm) {  // unblocks the stuck collective so the stream can drain
+                    ncclCommAbort(e->comm);
+                    e->comm = nullptr;
+                }
+                fail(LP_ERR_WORKER_FAILURE, "step " + std::to_string(e->last_step) + ": the step did not complete within " +
+                                                std::to_string(timeout_ms) + " ms (a peer rank is dead or stalled)");
+            }
+            std::this_thread::sleep_for(std::chrono::microseconds(200));
+        }
+        if (e->peer) {
+            unsigned status[2] = {0, 0};
+            LP_CUDA(cudaMemcpy(status, e->arena + e->status_off, sizeof(status), cudaMemcpyDeviceToHost));
+            if (status[0]) {
+                LP_CUDA(cudaMemset(e->arena + e->status_off, 0, sizeof(status)));
+                fail(LP_ERR_WORKER_FAILURE, failed_workers(e, status[0], static_cast<int>(status[1])) +
+                                                ": its epsilon shard never arrived over the peer exchange (watchdog); "
+                                                "z was left at the previous step");
+            }
+        }
+    });
+}
+
+int lp_engine_exchange_bench(lp_engine* e, int32_t step, int32_t iters, void* stream, double* ms_out,
+                             uint64_t* bytes_out) {
+    return guard([&] {
+        if (!e->peer && !e->comm) fail(LP_ERR_INVALID_ARGUMENT, "exchange bench needs a peer attach or an NCCL communicator");
+        if (e->M > 1) fail(LP_ERR_INVALID_GROUPING, "exchange bench is for plain LP engines");
+        if (iters < 1) fail(LP_ERR_INVALID_ARGUMENT, "iters must be >= 1");
+        cudaStream_t st = as_stream(stream);
+        const uint64_t pb = e->peer_bytes;
+        cudaEvent_t a = nullptr, b = nullptr;
+        LP_CUDA(cudaEventCreate(&a));
+        LP_CUDA(cudaEventCreate(&b));
+        LP_CUDA(cudaEventRecord(a, st));
+        for (int it = 0; it < iters; ++it) {
+            if (e->peer) {  // the unfused push (copy + signal + wait) of the step's full slot
+                ++e->epoch;
+                e->gather = e->arena + static_cast<size_t>(e->epoch & 1) * e->gather_bytes;
+                step_exchange_peer(e, step, st, false);
+            } else {
+                step_exchange(e, step, st);
+            }
+        }
+        LP_CUDA(cudaEventRecord(b, st));
+        LP_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        LP_CUDA(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        e->peer_bytes = pb;
+        const ShardLayout& L = e->layout[step_axis(e, step)];
+        *ms_out = ms;
+        *bytes_out = static_cast<uint64_t>(L.slot_elems) * e->cfg.dtype_bytes * (e->cfg.world - 1) * iters;
     });
 }
 

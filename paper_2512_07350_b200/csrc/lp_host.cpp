@@ -1,6 +1,7 @@
 // lp_host.cpp — host LP core + its C-ABI (plan builder, weights, layouts,
 // accounting, quantizer, synthetic inputs).  Compiled with -ffp-contract=off so
 // every double op rounds separately, as in the reference build.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -140,19 +141,41 @@ std::vector<double> weight_sums(const lp_plan& p) {
     return z;
 }
 
-ShardLayout shard_layout(const lp_plan& p, const Shape4& s, int world, int rank) {
+ShardLayout shard_layout(const lp_plan& p, const Shape4& s, int world, int rank, const AssignCost* cost) {
     if (world < 1 || rank < 0 || rank >= world) fail(LP_ERR_INVALID_ARGUMENT, "bad world/rank");
     const std::vector<i64> n = entry_elems(p, s);
+    std::vector<int> owner(n.size(), 0);
+    for (int k = 0; k < p.n_entries; ++k) owner[k] = k % world;  // round-robin (the default)
+    if (cost && p.n_entries > world) {
+        // balanced: longest-processing-time greedy over the per-entry cost model (the
+        // reference leaves the worker -> device mapping open; its workers are threads)
+        std::vector<int> order(n.size());
+        for (int k = 0; k < p.n_entries; ++k) order[k] = k;
+        auto c = [&](int k) { return cost->lin * static_cast<double>(n[k]) + cost->quad * static_cast<double>(n[k]) * static_cast<double>(n[k]); };
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return c(a) > c(b); });
+        std::vector<double> load(static_cast<size_t>(world), 0.0);
+        for (int k : order) {
+            int best = 0;
+            for (int r = 1; r < world; ++r)
+                if (load[r] < load[best]) best = r;
+            owner[k] = best;
+            load[best] += c(k);
+        }
+    }
     std::vector<i64> per_rank(static_cast<size_t>(world), 0), within(n.size(), 0);
-    for (int k = 0; k < p.n_entries; ++k) {
-        within[k] = per_rank[k % world];
-        per_rank[k % world] += n[k];
+    for (int k = 0; k < p.n_entries; ++k) {  // each rank's slot packs its entries in worker order
+        within[k] = per_rank[owner[k]];
+        per_rank[owner[k]] += n[k];
     }
     ShardLayout L;
     for (int r = 0; r < world; ++r) L.slot_elems = std::max(L.slot_elems, per_rank[r]);
+    // slots start on 16-byte boundaries for every storage width (8 elements >= 16 B), so the
+    // peer exchange's 16-B vector copies of rank r's slot [r*slot, (r+1)*slot) are aligned
+    L.slot_elems = (L.slot_elems + 7) / 8 * 8;
     for (int k = 0; k < p.n_entries; ++k) {
-        if (k % world == rank) L.owned.push_back(k);
-        L.base.push_back(static_cast<i64>(k % world) * L.slot_elems + within[k]);
+        if (owner[k] == rank) L.owned.push_back(k);
+        L.base.push_back(static_cast<i64>(owner[k]) * L.slot_elems + within[k]);
+        L.owner.push_back(owner[k]);
     }
     return L;
 }
@@ -344,6 +367,25 @@ int lp_shard_bases(const lp_plan* plan, const int64_t shape[4], int world, int64
     return guard([&] {
         const ShardLayout L = shard_layout(*plan, Shape4::from(shape), world, 0);
         for (size_t k = 0; k < L.base.size(); ++k) base_out[k] = L.base[k];
+    });
+}
+
+int lp_shard_layout_ex(const lp_plan* plan, const int64_t shape[4], int world, int rank, int32_t policy, double lin,
+                       double quad, int32_t* owned_out, int32_t* n_owned_out, int64_t* slot_elems_out,
+                       int32_t* owner_out, int64_t* base_out) {
+    return guard([&] {
+        if (policy != LP_ASSIGN_ROUND_ROBIN && policy != LP_ASSIGN_BALANCED)
+            fail(LP_ERR_INVALID_ARGUMENT, "assignment policy must be 0 (round-robin) or 1 (balanced)");
+        const AssignCost cost{lin, quad};
+        const ShardLayout L = shard_layout(*plan, Shape4::from(shape), world, rank, policy ? &cost : nullptr);
+        if (owned_out)
+            for (size_t i = 0; i < L.owned.size(); ++i) owned_out[i] = L.owned[i];
+        if (n_owned_out) *n_owned_out = static_cast<int32_t>(L.owned.size());
+        if (slot_elems_out) *slot_elems_out = L.slot_elems;
+        for (size_t k = 0; k < L.base.size(); ++k) {
+            if (owner_out) owner_out[k] = L.owner[k];
+            if (base_out) base_out[k] = L.base[k];
+        }
     });
 }
 

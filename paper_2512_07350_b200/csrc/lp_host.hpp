@@ -54,10 +54,18 @@ std::vector<double> weight_sums(const lp_plan& p);
 
 struct ShardLayout {
     std::vector<int> owned;      // entry ids (0-based) this rank computes, ascending
-    i64 slot_elems = 0;          // padded per-rank slot of the all-gather buffer
+    i64 slot_elems = 0;          // padded per-rank slot of the all-gather buffer (multiple of 8 elements)
     std::vector<i64> base;       // per entry: element offset in the gathered buffer
+    std::vector<int> owner;      // per entry: the rank that computes it
 };
-ShardLayout shard_layout(const lp_plan& p, const Shape4& s, int world, int rank);
+// Per-entry cost model of the balanced assignment: cost = lin*elems + quad*elems^2
+// (the DiT: linear layers ~ tokens, self-attention ~ tokens^2).
+struct AssignCost {
+    double lin = 1.0, quad = 0.0;
+};
+// Entries -> ranks: round-robin (entry e -> rank e % world) when cost is null, else
+// longest-processing-time greedy on the cost model (ties -> lowest rank).
+ShardLayout shard_layout(const lp_plan& p, const Shape4& s, int world, int rank, const AssignCost* cost = nullptr);
 
 void validate_plan(const lp_plan& p);
 double host_quantize(double v, int dtype_bytes);

@@ -289,8 +289,8 @@ void slice_to(const void* z, const Shape4& s, int axis, i64 begin, i64 end, int 
 // same offset of every peer's buffer with 16-B remote stores, then the last block to finish
 // (a grid-wide arrival counter) publishes `epoch` into every peer's flag word for rank r
 // with a system-scope release.  k_peer_wait: spins (system-scope acquire) until every peer's
-// flag for this rank's buffer reaches `epoch`; a 10 s clock64 watchdog raises
-// LP_FLAG_PEER_TIMEOUT instead of hanging.  The gather buffer is double-buffered by epoch
+// flag for this rank's buffer reaches `epoch`; a wall-time watchdog (peer_timeout_ms) raises
+// LP_FLAG_PEER_TIMEOUT and records the missing ranks instead of hanging.  The gather buffer is double-buffered by epoch
 // parity, so a push for step i+1 never lands in a buffer a peer's K10 of step i still reads.
 // ---------------------------------------------------------------------------
 constexpr unsigned LP_FLAG_PEER_TIMEOUT = 4u;
@@ -322,19 +322,32 @@ __global__ void __launch_bounds__(256) k_peer_push(const __grid_constant__ PeerP
         const unsigned done = atomicAdd(counter, 1u);
         if (done == gridDim.x - 1) {
             __threadfence_system();
-            for (int j = 0; j < pp.npeers; ++j) st_release_sys(pp.peer_flag[j], pp.epoch);
+            const unsigned long long ep = *pp.epoch + 1;
+            for (int j = 0; j < pp.npeers; ++j) st_release_sys(pp.peer_flag[j], ep);
+            *pp.epoch = ep;
             *counter = 0;
         }
     }
 }
 
-__global__ void k_peer_wait(const unsigned long long* flags, int world, int rank, unsigned long long epoch) {
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void k_peer_wait(const unsigned long long* flags, int world, int rank, const unsigned long long* epoch_p,
+                            unsigned* status, int step, unsigned long long timeout_ns) {
     const int j = threadIdx.x;
     if (j >= world || j == rank) return;
-    const long long t0 = clock64();
+    const unsigned long long epoch = *epoch_p;
+    const unsigned long long t0 = global_ns();
     while (ld_acquire_sys(flags + j) < epoch) {
-        if (clock64() - t0 > (1ll << 35)) {  // ~10-20 s: a dead peer, not a slow one
+        if (global_ns() - t0 > timeout_ns) {  // a dead or stalled peer, not a slow one
             raise_flag(LP_FLAG_PEER_TIMEOUT);
+            atomicOr(status, 1u << j);
+            status[1] = static_cast<unsigned>(step);
+            __threadfence();
             return;
         }
         __nanosleep(200);
@@ -347,8 +360,11 @@ void peer_push(const PeerPush& pp, unsigned* counter, cudaStream_t st) {
     LP_LAUNCH_CHECK();
 }
 
-void peer_wait(const unsigned long long* flags, int world, int rank, unsigned long long epoch, cudaStream_t st) {
-    k_peer_wait<<<1, 32 * ((world + 31) / 32), 0, st>>>(flags, world, rank, epoch);
+void peer_wait(const unsigned long long* flags, int world, int rank, const unsigned long long* epoch,
+               unsigned* status, int step, cudaStream_t st) {
+    // watchdog in wall time (%globaltimer): knob peer_timeout_ms, default 20 s
+    const unsigned long long ns = 1000000ull * static_cast<unsigned long long>(std::max(1, tune_get("peer_timeout_ms", 20000)));
+    k_peer_wait<<<1, 32 * ((world + 31) / 32), 0, st>>>(flags, world, rank, epoch, status, step, ns);
     LP_LAUNCH_CHECK();
 }
 
@@ -474,11 +490,17 @@ __device__ __forceinline__ double entry_weight(const ReconEntry& e, int64_t j) {
     return 1.0;
 }
 
+// A peer's shard never arrived (peer exchange watchdog): leave z as it was.
+__device__ __forceinline__ bool recon_aborted(const ReconParams& p) {
+    return p.abort != nullptr && *reinterpret_cast<const volatile unsigned*>(p.abort) != 0u;
+}
+
 template <int D, bool UPDATE, bool FAST>
 __global__ void __launch_bounds__(256) k_reconstruct(const __grid_constant__ ReconParams p,
                                                      const typename Store<D>::T* __restrict__ preds,
                                                      typename Store<D>::T* __restrict__ z,
                                                      typename Store<D>::T* __restrict__ eps_out) {
+    if (recon_aborted(p)) return;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < p.total;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = idx % p.inner;
@@ -538,6 +560,7 @@ __global__ void __launch_bounds__(256) k_reconstruct_tab(const __grid_constant__
                                                          const typename Store<D>::T* __restrict__ preds,
                                                          typename Store<D>::T* __restrict__ z,
                                                          typename Store<D>::T* __restrict__ eps_out) {
+    if (recon_aborted(p)) return;
     extern __shared__ double wt[];  // [n][Dx] weights, then [Dx] sums
     const int Dx = static_cast<int>(p.D), n = p.n;
     double* zsum = wt + n * Dx;
@@ -666,6 +689,7 @@ __global__ void __launch_bounds__(256) k_reconstruct_cov(const __grid_constant__
                                                          typename Store<D>::T* __restrict__ z,
                                                          typename Store<D>::T* __restrict__ eps_out,
                                                          const uint4* __restrict__ table, uint32_t table_vecs) {
+    if (recon_aborted(p)) return;
     using T = typename Store<D>::T;
     extern __shared__ __align__(16) double cov[];
     const int Dx = static_cast<int>(p.D);
@@ -792,6 +816,7 @@ __global__ void __launch_bounds__(256) k_reconstruct_xs(const __grid_constant__ 
                                                         typename Store<D>::T* __restrict__ z,
                                                         typename Store<D>::T* __restrict__ eps_out,
                                                         const void* __restrict__ table, uint32_t live) {
+    if (recon_aborted(p)) return;
     using T = typename Store<D>::T;
     const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= live) return;
@@ -885,10 +910,16 @@ static const void* recon_table(const ReconParams& p, size_t bytes, cudaStream_t 
     std::lock_guard<std::mutex> lock(mu);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    LP_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+        fail(LP_ERR_INVALID_ARGUMENT, "K10 coverage table must be built by an eager launch before graph capture");
     void* t = nullptr;
     LP_CUDA(cudaMalloc(&t, bytes));
     k_recon_table<<<1, 256, 0, st>>>(p, t);
     LP_LAUNCH_CHECK();
+    // published only once built: a caller on another stream may use it right away
+    LP_CUDA(cudaStreamSynchronize(st));
     cache.emplace(std::move(key), t);
     return t;
 }

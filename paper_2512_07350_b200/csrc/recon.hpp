@@ -27,6 +27,9 @@ struct ReconParams {
     double eta;
     FastDiv div_inner, div_d;  // valid (use32) when total < 2^31
     int use32;
+    // peer exchange: the engine's failure word (non-zero = a peer's shard never arrived);
+    // K10 then leaves z untouched instead of blending stale shards.  nullptr = no check.
+    const unsigned* abort;
     ReconEntry e[kMaxKernelEntries];
 };
 
@@ -45,10 +48,15 @@ struct PeerPush {
     uint8_t* peer[kMaxPeers];                  // the peers' gather buffers (same parity)
     unsigned long long* peer_flag[kMaxPeers];  // &flags_of_peer[rank]
     uint64_t off, bytes;                       // this rank's slot
-    unsigned long long epoch;
+    // the exchange epoch lives on the device (so a CUDA graph of the step can be replayed):
+    // the push kernel publishes *epoch + 1 and stores it back; the wait kernel waits for it
+    unsigned long long* epoch;
     int npeers;
 };
 void peer_push(const PeerPush& pp, unsigned* counter, cudaStream_t st);
-void peer_wait(const unsigned long long* flags, int world, int rank, unsigned long long epoch, cudaStream_t st);
+// status[0] |= 1 << j for every peer j whose flag did not reach `epoch` within the watchdog,
+// status[1] = step (the engine reports WorkerFailure from it, src/cluster.cpp:149-161).
+void peer_wait(const unsigned long long* flags, int world, int rank, const unsigned long long* epoch,
+               unsigned* status, int step, cudaStream_t st);
 
 }  // namespace lpb200

@@ -246,6 +246,18 @@ def cost_report(steps, workers, overlap_ratio, dims, patch, preset="wan21-like",
     return d
 
 
+def shard_layout_ex(plan: PartitionPlan, dims, world: int, rank: int, policy="round-robin", lin=1.0, quad=0.0):
+    """lp_shard_layout_ex: (owned entries, slot_elems, owner per entry, base per entry)."""
+    n = plan.workers
+    owned = (C.c_int32 * _lib.LP_MAX_WORKERS)()
+    cnt, slot = C.c_int32(), C.c_int64()
+    owner, base = (C.c_int32 * n)(), (C.c_int64 * n)()
+    check(lib().lp_shard_layout_ex(C.byref(plan.raw), i64arr(dims), world, rank,
+                                   {"round-robin": 0, "balanced": 1}[policy], float(lin), float(quad), owned,
+                                   C.byref(cnt), C.byref(slot), owner, base))
+    return list(owned[:cnt.value]), slot.value, list(owner), list(base)
+
+
 def step_comm_bytes(plan: PartitionPlan, dims, wire_bytes: int, world: int, dtype_bytes: int):
     a, b = C.c_uint64(), C.c_uint64()
     check(lib().lp_step_comm_bytes(C.byref(plan.raw), i64arr(dims), wire_bytes, world, dtype_bytes, C.byref(a),
@@ -466,7 +478,8 @@ class LpEngine:
 
     def __init__(self, dims, patch, dtype_bytes, workers, overlap_ratio, steps, eta, guidance, cond,
                  denoiser="box", radius=(1, 1, 1), wire_bytes=2, world=1, rank=0, nccl_id=None, mode="exact",
-                 dit: DiTDenoiser | None = None, t_coeff=0.01, cond_coeff=0.1, schedule=None, group_size=1):
+                 dit: DiTDenoiser | None = None, t_coeff=0.01, cond_coeff=0.1, schedule=None, group_size=1,
+                 assign="round-robin"):
         cfg = _lib.EngineConfig()
         for i in range(4):
             cfg.shape[i] = int(dims[i])
@@ -491,6 +504,7 @@ class LpEngine:
         cfg.rank = rank
         cfg.dit = dit.handle if dit is not None else None
         cfg.group_size = int(group_size)
+        cfg.assign = {"round-robin": 0, "balanced": 1}[assign]
         if schedule:
             axes = parse_schedule(schedule)
             cfg.schedule_len = len(axes)
@@ -520,6 +534,19 @@ class LpEngine:
     def run(self, first_step, count, stream=None):
         st = C.c_void_p(stream) if stream is not None else _stream()
         check(lib().lp_engine_run(self.handle, first_step, count, st))
+
+    def sync(self, timeout_s=0.0, stream=None):
+        """lp_engine_sync: wait for the enqueued steps; a dead/stalled peer or an NCCL async
+        error raises LpError(WorkerFailure) naming the step (and the worker, for the peer path)."""
+        st = C.c_void_p(stream) if stream is not None else _stream()
+        check(lib().lp_engine_sync(self.handle, st, int(timeout_s * 1000)))
+
+    def exchange_bench(self, step, iters, stream=None):
+        """lp_engine_exchange_bench: (ms, bytes received by this rank) of `iters` K9 exchanges."""
+        st = C.c_void_p(stream) if stream is not None else _stream()
+        ms, nb = C.c_double(), C.c_uint64()
+        check(lib().lp_engine_exchange_bench(self.handle, int(step), int(iters), st, C.byref(ms), C.byref(nb)))
+        return ms.value, int(nb.value)
 
     def step_phase(self, step, phase, stream=None):
         """lp_engine_step_phase: 1 = compute this rank's shards, 2 = NCCL exchange, 3 = reconstruct."""

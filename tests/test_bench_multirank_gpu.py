@@ -26,5 +26,22 @@ def test_bench_two_ranks_peer_exchange(cuda):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["exchange"] == "peer"
     assert d["value"] > 0 and d["e2e"]["value"] > 0
-    assert d["comm"]["nccl_bytes_per_step_measured_all_ranks"] > 0
-    assert d["allgather"]["launches"] > 0
+    assert d["comm"]["exchange_bytes_per_step_measured_all_ranks"] > 0
+    assert d["allgather"]["in_step_launches"] > 0
+    assert len(d["ranks"]) == 2 and all(r["exchange_bench"]["GBps"] > 0 for r in d["ranks"])
+
+
+@pytest.mark.gpu
+def test_bench_gpus_2_launches_its_own_ranks(cuda):
+    """`python bench.py --gpus 2` WITHOUT torchrun starts both ranks itself (the driver's
+    command line); under LP_BENCH_GLOO_TEST both sit on GPU 0."""
+    env = dict(os.environ, LP_BENCH_GLOO_TEST="1")
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, "bench.py", "--gpus", "2", "--steps", "2", "--warmup", "3", "--layers", "2"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["exchange"] == "peer" and [x["rank"] for x in d["ranks"]] == [0, 1]
+    assert d["scaling_model"]["flop_ideal_speedup_vs_1gpu"] > 1.5

@@ -152,6 +152,28 @@ def test_engine_dit_step_runs(cuda):
     assert eng.launches() > 0
 
 
+def test_engine_dit_remainder_shard_shapes(cuda):
+    """Shards that keep the reference's remainder rows (H=17 with patch 2) need ceil(H/p) token
+    rows: the engine reserves the DiT workspace with the DiT's own patch and ceil division
+    (ADVICE r1), so the forward never exceeds its reservation."""
+    dims = (16, 5, 17, 16)
+    z, cond = lp.synthetic_latent(dims, 4, 2025)
+    dit = lp.DiTDenoiser(cond, num_layers=1)
+    eng = lp.LpEngine(dims, (1, 2, 2), 4, 2, 0.5, 3, 0.05, 5.0, cond, denoiser="dit", dit=dit)
+    eng.load(z)
+    eng.run(1, 3)
+    eng.sync(timeout_s=120)
+    assert torch.isfinite(eng.z.data).all()
+    eng.close()
+    # an LP patch coarser than the DiT's: (1,4,4) LP windows on a (1,2,2) DiT
+    eng = lp.LpEngine(dims, (1, 4, 4), 4, 2, 0.5, 3, 0.05, 5.0, cond, denoiser="dit", dit=dit)
+    eng.load(z)
+    eng.run(1, 3)
+    eng.sync(timeout_s=120)
+    assert torch.isfinite(eng.z.data).all()
+    eng.close()
+
+
 def test_lp_loop_with_dit_matches_reference_run_lp(cuda, reference):
     """The UNMODIFIED reference run_lp (oracle/_ref) driving the fp32 torch DiT through its
     Denoiser plugin slot, vs our engine (bf16 tcgen05 DiT, CFG batch 2, K1/K10 kernels).

@@ -204,3 +204,40 @@ def test_cost_report_matches_reference(reference):
     assert round(c2["C_LP_exact"] / 1e6, 1) == 1162.7 and round(c2["C_NMP"] / 1e6, 1) == 30191.6
     paper = lp.cost_report(60, 4, 0.5, (16, 13, 60, 104), (1, 2, 2))
     assert round(paper["ratio_exact"], 4) == 0.0381
+
+
+def test_shard_layout_alignment_and_balanced_assignment():
+    """Slots start 16-B aligned for every dtype (slot_elems % 8 == 0), round-robin is the
+    default, and the balanced policy is longest-processing-time greedy on the cost model."""
+    dims = (16, 21, 60, 104)
+    for step in (1, 2, 3):
+        for K in (4, 8):
+            plan = lp.build_plan(dims, (1, 2, 2), step, K, 0.5)
+            offs = plan.offsets(dims)
+            n = [offs[k + 1] - offs[k] for k in range(plan.workers)]
+            for world in (1, 2, 3, 4, 8):
+                owned, slot = lp.shard_layout(plan, dims, world, 0)
+                assert slot % 8 == 0
+                o2, s2, owner, base = lp.shard_layout_ex(plan, dims, world, 0, "round-robin")
+                assert (o2, s2) == (owned, slot) and owner == [k % world for k in range(plan.workers)]
+                lin, quad = 1.0, 1e-6
+                _, sb, ob, bb = lp.shard_layout_ex(plan, dims, world, 0, "balanced", lin, quad)
+                cost = [lin * x + quad * x * x for x in n]
+                load, want = [0.0] * world, [0] * plan.workers
+                if plan.workers <= world:
+                    want = list(range(plan.workers))
+                else:
+                    for k in sorted(range(plan.workers), key=lambda k: -cost[k]):
+                        r = min(range(world), key=lambda r: load[r])
+                        want[k] = r
+                        load[r] += cost[k]
+                assert ob == want
+                assert sb % 8 == 0
+                spans = sorted((bb[k], bb[k] + n[k]) for k in range(plan.workers))
+                assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
+                assert all(ob[k] * sb <= bb[k] and bb[k] + n[k] <= (ob[k] + 1) * sb for k in range(plan.workers))
+    # a one-channel latent whose per-rank sums are not multiples of 8 still gets aligned slots
+    plan = lp.build_plan((1, 5, 6, 6), (1, 2, 2), 1, 4, 0.5)
+    for world in (2, 3):
+        _, slot = lp.shard_layout(plan, (1, 5, 6, 6), world, 1)
+        assert slot % 8 == 0

@@ -28,11 +28,12 @@ def rel(a, b):
     return float((a.float() - b.float()).norm() / b.float().norm())
 
 
-def ctx_kv(dit):
-    L = dit.cfg.num_layers
-    ck = [dit.debug_tensor(f"ctx_k.{l}", torch.bfloat16).float().view(2, dit.cfg.text_len, -1) for l in range(L)]
-    cv = [dit.debug_tensor(f"ctx_v.{l}", torch.bfloat16).float().view(2, dit.cfg.text_len, -1) for l in range(L)]
-    return ck, cv
+def oracle_dit(dit, cond):
+    """The oracle's own DiT (weights, text, cross K/V regenerated: oracle/dit_oracle.py)."""
+    from oracle.dit_oracle import OracleDiT
+
+    od = OracleDiT(dit.cfg, cond)
+    return od, *od.context_kv()
 
 
 def forward_case(shape, layers, t=37, w=5.0, seed=2025):
@@ -40,10 +41,10 @@ def forward_case(shape, layers, t=37, w=5.0, seed=2025):
     dit = lp.DiTDenoiser(cond, num_layers=layers)
     eps = dit.cfg_predict(z, t, w)
     torch.cuda.synchronize()
-    ck, cv = ctx_kv(dit)
+    od, ck, cv = oracle_dit(dit, cond)
     t0 = time.time()
-    want, _ = DiTReference(dit).forward(z.data.float(), t, ck, cv, w)
-    emul, _ = DiTReference(dit, act_bf16=True).forward(z.data.float(), t, ck, cv, w)
+    want, _ = DiTReference(od).forward(z.data.float(), t, ck, cv, w)
+    emul, _ = DiTReference(od, act_bf16=True).forward(z.data.float(), t, ck, cv, w)
     torch.cuda.synchronize()
     out = {"shape": list(shape), "layers": layers, "t": t, "w": w,
            "rel_l2_ours_vs_fp32": rel(eps.data, want), "rel_l2_bf16_operands_vs_fp32": rel(emul, want),
@@ -58,8 +59,8 @@ def trajectory_case(ref, dims, K, r, steps, eta=0.05, w=5.0, layers=2, seed=2025
     os.environ["LPSIM_THREADS"] = "0"
     z, cond = lp.synthetic_latent(dims, 4, seed)
     dit = lp.DiTDenoiser(cond, num_layers=layers)
-    ck, cv = ctx_kv(dit)
-    dr = DiTReference(dit)
+    od, ck, cv = oracle_dit(dit, cond)
+    dr = DiTReference(od)
 
     def predict(zz, t, c, is_null):
         return dr.predict(torch.from_numpy(zz).float().cuda(), t, ck, cv, 0 if is_null else 1).double().cpu().numpy()

@@ -104,9 +104,12 @@ class Cfg:
 
     def entry_flops(self, shape):
         """Algorithmic FLOPs of the CFG-batched DiT on one shard: GEMM 2MNK with M = 2n over QKV, O,
-        cross-Q, cross-O, FFN1, FFN2; self-attention 4 n^2 d per batch; cross-attention 4 n 512 d."""
+        cross-Q, cross-O, FFN1, FFN2; self-attention 4 n^2 d per batch; cross-attention 4 n 512 d;
+        minus block 0's self-attention sub-block of one half (QKV + O GEMMs, attention): both CFG
+        halves are identical there, so the engine computes it once (knob dit_dedupe0)."""
         n, d = self.tokens(shape), self.d
-        return self.layers * (2 * 2 * n * (6 * d * d + 2 * d * self.F) + 2 * 4 * n * n * d + 2 * 4 * n * 512 * d)
+        full = self.layers * (2 * 2 * n * (6 * d * d + 2 * d * self.F) + 2 * 4 * n * n * d + 2 * 4 * n * 512 * d)
+        return full - (2 * n * 4 * d * d + 4 * n * n * d)
 
     def cost_model(self):
         """lp_shard_layout_ex cost per element (balanced assignment): linear ~ n, attention ~ n^2."""

@@ -204,6 +204,12 @@ int lp_device_check(int device); /* LP_OK iff device exists and is sm_100 */
 /* Sticky device flags raised by kernels (1 = a stored value was non-finite:
  * the reference's NonFinite, src/latent.cpp:72-77).  Synchronizes. */
 int lp_device_flags(uint32_t* flags_out, int reset);
+/* Device memory for hosts that bind only this header (integration/ shim): cudaMalloc /
+ * cudaFree / synchronous cudaMemcpy on the current device.  Not for the hot path. */
+int lp_device_alloc(size_t bytes, void** out);
+int lp_device_free(void* p);
+int lp_copy_to_device(void* dst, const void* src, size_t bytes);
+int lp_copy_to_host(void* dst, const void* src, size_t bytes);
 /* Kernel launches issued by this library since load. */
 uint64_t lp_launch_count(void);
 /* Live per-kernel-class timing with CUDA events on the launching stream
@@ -313,6 +319,16 @@ int lp_dit_set_mirrors(lp_dit* dit, int32_t n, const int64_t* byte_deltas);
  * text), one forward, combine uncond + w*(cond-uncond), quantize to dtype. */
 int lp_dit_cfg_predict(lp_dit* dit, const void* sub, const int64_t shape[4], int dtype_bytes, int timestep,
                        double guidance, void* eps_out, void* stream);
+/* ONE CFG pass — Denoiser::predict (include/lpsim/denoise.hpp:35-36) of the DiT: null_text != 0
+ * uses the null (zero) text context (the uncond pass cfg_predict makes with
+ * ConditioningVector::null_like, src/denoise.cpp:29), else the synthetic cond text.  Writes
+ * the prediction quantized to dtype.  Bit-identical to the matching half of the CFG-batched
+ * forward, so the reference's own cfg_predict over two predict calls reproduces
+ * lp_dit_cfg_predict bit for bit. */
+int lp_dit_predict(lp_dit* dit, const void* sub, const int64_t shape[4], int dtype_bytes, int timestep,
+                   int32_t null_text, void* eps_out, void* stream);
+int lp_dit_predict_slot(lp_dit* dit, int32_t slot, const void* sub, const int64_t shape[4], int dtype_bytes,
+                        int timestep, int32_t null_text, void* eps_out, void* stream);
 /* For step loops captured into CUDA graphs: with time_on_device(1) the forwards read the
  * timestep from the slot's device scalar, which lp_dit_set_time writes (stream-ordered)
  * before each replay, instead of baking the host value into a kernel argument. */

@@ -119,6 +119,8 @@ _SIGS = {
     "lp_dit_destroy": (_i, [_vp]),
     "lp_dit_reserve": (_i, [_vp, _i64]),
     "lp_dit_cfg_predict": (_i, [_vp, _vp, _i64p, _i, _i, _d, _vp, _vp]),
+    "lp_dit_predict": (_i, [_vp, _vp, _i64p, _i, _i, _i32, _vp, _vp]),
+    "lp_dit_predict_slot": (_i, [_vp, _i32, _vp, _i64p, _i, _i, _i32, _vp, _vp]),
     "lp_dit_reserve_slots": (_i, [_vp, _i64, _i32]),
     "lp_dit_cfg_predict_slot": (_i, [_vp, _i32, _vp, _i64p, _i, _i, _d, _vp, _vp]),
     "lp_dit_num_params": (_i, [_vp]),

@@ -496,7 +496,7 @@ void rmsnorm_rope(__nv_bfloat16* buf, int64_t rows, int64_t ld, int64_t col0, in
 template <int D>
 __global__ void k_unpatchify_cfg(const float* __restrict__ head, typename Store<D>::T* __restrict__ eps, int C, int F,
                                  int H, int W, int pt, int ph, int pw, int nh, int nw, int64_t ntok, double w,
-                                 const __grid_constant__ EpsMirrors mr) {
+                                 int single, const __grid_constant__ EpsMirrors mr) {
     using T = typename Store<D>::T;
     const int64_t total = static_cast<int64_t>(C) * F * H * W;
     const int feat = C * pt * ph * pw;
@@ -508,9 +508,13 @@ __global__ void k_unpatchify_cfg(const float* __restrict__ head, typename Store<
         const int64_t tok = (static_cast<int64_t>(t / pt) * nh + y / ph) * nw + x / pw;
         const int fe = (((t % pt) * ph + (y % ph)) * pw + (x % pw)) * C + c;
         const double u = quantize_dev<D>(static_cast<double>(head[tok * feat + fe]));
-        const double cc = quantize_dev<D>(static_cast<double>(head[(ntok + tok) * feat + fe]));
         T q;
-        store_q<D>(&q, 0, __dadd_rn(u, __dmul_rn(w, __dsub_rn(cc, u))));
+        if (single) {  // one CFG pass (Denoiser::predict): the prediction, quantized
+            store_q<D>(&q, 0, u);
+        } else {
+            const double cc = quantize_dev<D>(static_cast<double>(head[(ntok + tok) * feat + fe]));
+            store_q<D>(&q, 0, __dadd_rn(u, __dmul_rn(w, __dsub_rn(cc, u))));
+        }
         eps[i] = q;
         // K8+K9 fused: the same ε̂ element stored straight into every peer's gather buffer
         // (CUDA-IPC mapped; remote stores over NVLink), at the same offset as the local slot
@@ -520,13 +524,13 @@ __global__ void k_unpatchify_cfg(const float* __restrict__ head, typename Store<
 }
 
 void unpatchify_cfg(const float* head, int dtype, const int shape[4], const int patch[3], double w, void* eps,
-                    cudaStream_t st, const EpsMirrors& mr) {
+                    cudaStream_t st, const EpsMirrors& mr, bool single) {
     const int nh = (shape[2] + patch[1] - 1) / patch[1], nw = (shape[3] + patch[2] - 1) / patch[2];
     const int nf = (shape[1] + patch[0] - 1) / patch[0];
     const int64_t ntok = static_cast<int64_t>(nf) * nh * nw;
     const int64_t total = static_cast<int64_t>(shape[0]) * shape[1] * shape[2] * shape[3];
     const int g = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-#define LP_UNP(DD) k_unpatchify_cfg<DD><<<g, 256, 0, st>>>(head, static_cast<typename Store<DD>::T*>(eps), shape[0], shape[1], shape[2], shape[3], patch[0], patch[1], patch[2], nh, nw, ntok, w, mr)
+#define LP_UNP(DD) k_unpatchify_cfg<DD><<<g, 256, 0, st>>>(head, static_cast<typename Store<DD>::T*>(eps), shape[0], shape[1], shape[2], shape[3], patch[0], patch[1], patch[2], nh, nw, ntok, w, single ? 1 : 0, mr)
     if (dtype == 2) LP_UNP(2);
     else if (dtype == 4) LP_UNP(4);
     else LP_UNP(8);

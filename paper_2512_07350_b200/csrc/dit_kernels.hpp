@@ -43,7 +43,9 @@ struct EpsMirrors {
     int n = 0;
     int64_t delta[16] = {};
 };
+// single: `head` holds ONE pass (batch 1) and eps = quantize(prediction) (Denoiser::predict);
+// else rows [0, ntok) are the uncond pass, [ntok, 2 ntok) the cond pass, combined as cfg_predict.
 void unpatchify_cfg(const float* head, int dtype, const int shape[4], const int patch[3], double w, void* eps,
-                    cudaStream_t st, const EpsMirrors& mr = EpsMirrors());
+                    cudaStream_t st, const EpsMirrors& mr = EpsMirrors(), bool single = false);
 
 }  // namespace lpb200

@@ -1102,6 +1102,28 @@ int lp_device_flags(uint32_t* flags_out, int reset) {
 
 uint64_t lp_launch_count(void) { return launch_count(); }
 
+// Device memory plumbing for hosts that bind only this header (the reference-side shim in
+// integration/): no cuda_runtime.h needed on the caller's side.
+int lp_device_alloc(size_t bytes, void** out) {
+    return guard([&] {
+        *out = nullptr;
+        if (bytes) LP_CUDA(cudaMalloc(out, bytes));
+    });
+}
+int lp_device_free(void* p) {
+    return guard([&] { LP_CUDA(cudaFree(p)); });
+}
+int lp_copy_to_device(void* dst, const void* src, size_t bytes) {
+    return guard([&] {
+        if (bytes) LP_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    });
+}
+int lp_copy_to_host(void* dst, const void* src, size_t bytes) {
+    return guard([&] {
+        if (bytes) LP_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    });
+}
+
 int lp_extract(const lp_plan* plan, int32_t first, int32_t count, const void* z, const int64_t shape[4], int dtype,
                void* dst, void* stream) {
     return guard([&] {

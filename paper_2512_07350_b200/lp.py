@@ -427,6 +427,14 @@ class DiTDenoiser:
                                        float(guidance), out.ptr(), _stream()))
         return out
 
+    def predict(self, z: LatentTensor, timestep: int, null_text: bool = False) -> LatentTensor:
+        """Denoiser::predict: ONE CFG pass (null text = the uncond pass), quantized to z's dtype."""
+        self.reserve(self.tokens(z.shape))
+        out = LatentTensor.empty(z.shape, z.dtype_bytes)
+        check(lib().lp_dit_predict(self.handle, z.ptr(), i64arr(z.shape), z.dtype_bytes, int(timestep),
+                                   1 if null_text else 0, out.ptr(), _stream()))
+        return out
+
     def params(self):
         torch = _torch()
         out = {}

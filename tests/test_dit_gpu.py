@@ -154,6 +154,50 @@ def test_dit_params_bit_exact_vs_oracle_generator(cuda, kw):
         assert torch.equal(v.view(iv), o.view(iv)), n
 
 
+@pytest.mark.parametrize("d", [2, 4, 8])
+def test_dit_single_pass_predict_reproduces_cfg_batch(cuda, d):
+    """Denoiser::predict of the DiT (one CFG pass, lp_dit_predict) is bit-identical to the matching
+    half of the CFG-batched forward: the reference's cfg_predict over two predict calls
+    (src/denoise.cpp:24-39: u + w (c - u) in fp64 over quantized passes, quantized) equals the
+    fused lp_dit_cfg_predict bit for bit, in every storage dtype."""
+    z, cond = lp.synthetic_latent((16, 5, 16, 16), d, 2025)
+    dit = lp.DiTDenoiser(cond, num_layers=2)
+    t, w = 37, 5.0
+    fused = dit.cfg_predict(z, t, w).to_numpy()
+    u = dit.predict(z, t, null_text=True).to_numpy()
+    c = dit.predict(z, t, null_text=False).to_numpy()
+    want = lp._quantize_np(u + w * (c - u), d)
+    assert np.array_equal(fused, want)
+    assert not np.array_equal(u, c)
+
+
+def test_dit_single_pass_predict_vs_oracle(cuda):
+    from tests.dit_reference import DiTReference
+
+    z, cond = lp.synthetic_latent((16, 5, 16, 16), 4, 2025)
+    dit = lp.DiTDenoiser(cond, num_layers=2)
+    od, ck, cv = _oracle_ctx(dit, cond)
+    ref = DiTReference(od)
+    for b in (0, 1):
+        got = dit.predict(z, 21, null_text=(b == 0)).data.float()
+        want = ref.predict(z.data.float(), 21, ck, cv, b).float()
+        rel = ((got - want).norm() / want.norm()).item()
+        assert np.isfinite(rel) and rel <= 5e-2, (b, rel)
+
+
+def test_block0_self_attention_dedupe_is_bit_identical(cuda):
+    """Block 0's self-attention sub-block runs once for the two identical CFG halves (knob
+    dit_dedupe0); the result equals the duplicated computation bit for bit."""
+    z, cond = lp.synthetic_latent((16, 5, 16, 16), 4, 2025)
+    dit = lp.DiTDenoiser(cond, num_layers=2)
+    outs = []
+    for on in (0, 1):
+        _lib.check(_lib.lib().lp_tune(b"dit_dedupe0", on))
+        outs.append(dit.cfg_predict(z, 9, 5.0).data.clone())
+    _lib.check(_lib.lib().lp_tune(b"dit_dedupe0", 1))
+    assert torch.equal(outs[0], outs[1])
+
+
 def test_text_context_kv_all_layers_vs_oracle(cuda):
     """The cached cross-attention K/V of all 30 layers, uncond (null text) and cond (synthetic
     text) halves, vs the oracle's fp32 restatement: its own text generator, text MLP, K/V

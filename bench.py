@@ -527,6 +527,12 @@ def run_ours(args, rank, world, local_rank):
     L.lp_tune(b"engine_serial", 0)
     prof_ms = pe0.elapsed_time(pe1)
     _lib.check(L.lp_profile_collect(nl, kms, kfl, kby))
+    # ---- K1 / K10 alone (HBM roofline): back-to-back replays per axis of the cycle ----
+    hb = {}
+    for s in range(first, first + ncyc):
+        ax = "THW"[cfg.axis_of(step_index(s))]
+        if ax not in hb:
+            hb[ax] = eng.hbm_bench(step_index(s), args.hbm_iters, args.hbm_sets)
 
     # ---- per-rank report ----
     owned = {}
@@ -555,10 +561,21 @@ def run_ours(args, rank, world, local_rank):
         pass
     peaks_hbm = peaks.get("hbm_gbs") or 7700.0
     hbm = {}
-    for i, nm in ((4, "k1_gather"), (5, "k10_reconstruct_update")):
-        gbps = kby[i] / kms[i] / 1e6 if kms[i] else None
-        hbm[nm] = {"launches": int(nl[i]), "ms": kms[i], "algorithmic_bytes": kby[i], "GBps": gbps,
-                   "frac_of_hbm": gbps / peaks_hbm if gbps else None, "share_of_step": kms[i] / prof_ms if prof_ms else None}
+    for i, nm, key in ((4, "k1_gather", "k1"), (5, "k10_reconstruct_update", "k10")):
+        per_axis = {}
+        for ax, r in hb.items():
+            gbps = r[key + "_bytes"] / r[key + "_ms"] / 1e6 if r[key + "_ms"] else None
+            per_axis[ax] = {"us_per_launch": 1000.0 * r[key + "_ms"], "algorithmic_bytes": r[key + "_bytes"],
+                            "GBps": gbps, "frac_of_hbm": gbps / peaks_hbm if gbps else None}
+        tb = sum(r[key + "_bytes"] for r in hb.values())
+        tm = sum(r[key + "_ms"] for r in hb.values())
+        hbm[nm] = {"per_axis": per_axis, "GBps": tb / tm / 1e6 if tm else None,
+                   "frac_of_hbm": tb / tm / 1e6 / peaks_hbm if tm else None,
+                   "share_of_step": kms[i] / prof_ms if prof_ms else None,
+                   "in_step_event_timed": {"launches": int(nl[i]), "ms": kms[i], "algorithmic_bytes": kby[i]}}
+    hbm["timing"] = (f"per axis: {args.hbm_iters} back-to-back launches over {args.hbm_sets} private buffer copies "
+                     f"used round robin (working set > L2, so launches stream from HBM), CUDA events around the "
+                     f"whole run on the launching stream; share_of_step from the serialised profiling cycle")
     hbm["peak_GBps"] = peaks_hbm
     hbm["peak_source"] = "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)" if peaks.get("hbm_gbs") else "fallback 7700"
     ag = None
@@ -692,6 +709,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-steps", type=int, default=0, help="reference arm: whole LP steps to time (default: one cycle)")
     ap.add_argument("--exchange-iters", type=int, default=20)
+    ap.add_argument("--hbm-iters", type=int, default=64, help="K1/K10 replays per axis for the HBM roofline")
+    ap.add_argument("--hbm-sets", type=int, default=8, help="buffer copies the K1/K10 replays cycle through")
     ap.add_argument("--sync-timeout", type=float, default=600.0, help="seconds before a stalled step is a WorkerFailure")
     ap.add_argument("--plan-only", action="store_true", help="print the N-rank assignment and FLOP-ideal bound (no GPU)")
     args = ap.parse_args()

@@ -447,6 +447,12 @@ int lp_engine_sync(lp_engine* e, void* stream, int64_t timeout_ms);
  * this rank received (slot x (world-1) x iters). */
 int lp_engine_exchange_bench(lp_engine* e, int32_t step, int32_t iters, void* stream, double* ms_out,
                              uint64_t* bytes_out);
+/* K1 and K10 alone, for their HBM roofline: `iters` back-to-back launches each of step's K1
+ * (gather of this rank's windows) and K10 (blend + sampler update of the full latent), on
+ * `sets` private copies of (z, shards, gathered ε̂) used round robin so consecutive launches
+ * stream from HBM, not L2.  out = {K1 ms per launch, K1 algorithmic bytes per launch, K10 ms
+ * per launch, K10 algorithmic bytes per launch}; the engine's own z is untouched. */
+int lp_engine_hbm_bench(lp_engine* e, int32_t step, int32_t iters, int32_t sets, void* stream, double out[4]);
 /* Bytes this engine moved over NCCL so far, and the reference ledger bytes. */
 int lp_engine_comm(const lp_engine* e, uint64_t* nccl_bytes, uint64_t* ledger_bytes);
 /* Kernel launches issued by the engine so far (this library's kernels only). */

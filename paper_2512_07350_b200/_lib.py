@@ -158,6 +158,7 @@ _SIGS = {
     "lp_engine_run": (_i, [_vp, _i32, _i32, _vp]),
     "lp_engine_sync": (_i, [_vp, _vp, _i64]),
     "lp_engine_exchange_bench": (_i, [_vp, _i32, _i32, _vp, _f64p, C.POINTER(C.c_uint64)]),
+    "lp_engine_hbm_bench": (_i, [_vp, _i32, _i32, _i32, _vp, _f64p]),
     "lp_engine_comm": (_i, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "lp_engine_launches": (_i, [_vp, C.POINTER(C.c_uint64)]),
 }

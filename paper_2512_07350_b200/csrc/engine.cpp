@@ -724,6 +724,58 @@ int lp_engine_exchange_bench(lp_engine* e, int32_t step, int32_t iters, void* st
     });
 }
 
+int lp_engine_hbm_bench(lp_engine* e, int32_t step, int32_t iters, int32_t sets, void* stream, double out[4]) {
+    return guard([&] {
+        if (iters < 1 || sets < 1) fail(LP_ERR_INVALID_ARGUMENT, "iters and sets must be >= 1");
+        if (e->M > 1) fail(LP_ERR_INVALID_GROUPING, "hbm bench is for plain LP engines");
+        cudaStream_t st = as_stream(stream);
+        const lp_engine_config& c = e->cfg;
+        const int a = step_axis(e, step), E = c.dtype_bytes;
+        const lp_plan& plan = e->plans[a];
+        const ShardLayout& L = e->layout[a];
+        const size_t zb = static_cast<size_t>(e->shape.volume()) * E;
+        size_t subb = 0, predb = 0;
+        for (int k : L.owned) subb += static_cast<size_t>(e->elems[a][k]) * E;
+        for (size_t k = 0; k < e->elems[a].size(); ++k) predb += static_cast<size_t>(e->elems[a][k]) * E;
+        const size_t gb = static_cast<size_t>(L.slot_elems) * E * c.world;
+        const size_t zs = (zb + 255) / 256 * 256, ss = (subb + 255) / 256 * 256, gs = (gb + 255) / 256 * 256;
+        // `sets` private copies of (z, sub, gather), used round robin, so with enough sets the
+        // working set of consecutive launches exceeds L2 and every launch streams from HBM
+        uint8_t* buf = nullptr;
+        LP_CUDA(cudaMalloc(&buf, (zs + ss + gs) * static_cast<size_t>(sets)));
+        auto zp = [&](int s) { return buf + static_cast<size_t>(s) * (zs + ss + gs); };
+        for (int s = 0; s < sets; ++s) {
+            LP_CUDA(cudaMemcpyAsync(zp(s), e->z, zb, cudaMemcpyDeviceToDevice, st));
+            LP_CUDA(cudaMemcpyAsync(zp(s) + zs + ss, e->gather, gb, cudaMemcpyDeviceToDevice, st));
+        }
+        cudaEvent_t ev[3] = {};
+        for (auto& x : ev) LP_CUDA(cudaEventCreate(&x));
+        auto k1 = [&](int s) {
+            if (!L.owned.empty())
+                gather_entries(zp(s), e->shape, plan, L.owned.data(), static_cast<int>(L.owned.size()), E, zp(s) + zs, st);
+        };
+        auto k10 = [&](int s) {
+            reconstruct_dispatch(e->recon[a], E, zp(s) + zs + ss, zp(s), nullptr, true, c.mode == LP_MODE_FAST, st);
+        };
+        for (int s = 0; s < sets; ++s) { k1(s); k10(s); }  // warm-up (and K10's coverage table)
+        LP_CUDA(cudaEventRecord(ev[0], st));
+        for (int it = 0; it < iters; ++it) k1(it % sets);
+        LP_CUDA(cudaEventRecord(ev[1], st));
+        for (int it = 0; it < iters; ++it) k10(it % sets);
+        LP_CUDA(cudaEventRecord(ev[2], st));
+        LP_CUDA(cudaEventSynchronize(ev[2]));
+        float m1 = 0.f, m2 = 0.f;
+        LP_CUDA(cudaEventElapsedTime(&m1, ev[0], ev[1]));
+        LP_CUDA(cudaEventElapsedTime(&m2, ev[1], ev[2]));
+        for (auto& x : ev) cudaEventDestroy(x);
+        LP_CUDA(cudaFree(buf));
+        out[0] = static_cast<double>(m1) / iters;
+        out[1] = 2.0 * static_cast<double>(subb);                // K1: read the windows, write them packed
+        out[2] = static_cast<double>(m2) / iters;
+        out[3] = static_cast<double>(predb) + 2.0 * zb;        // K10: every prediction once, z read + written
+    });
+}
+
 int lp_engine_comm(const lp_engine* e, uint64_t* nccl_bytes, uint64_t* ledger_bytes) {
     *nccl_bytes = e->nccl_bytes + e->peer_bytes;
     *ledger_bytes = e->ledger_bytes;

@@ -556,6 +556,14 @@ class LpEngine:
         check(lib().lp_engine_exchange_bench(self.handle, int(step), int(iters), st, C.byref(ms), C.byref(nb)))
         return ms.value, int(nb.value)
 
+    def hbm_bench(self, step, iters=50, sets=8, stream=None):
+        """lp_engine_hbm_bench: K1 / K10 of `step` replayed back to back over `sets` buffer copies.
+        Returns {"k1_ms", "k1_bytes", "k10_ms", "k10_bytes"} per launch."""
+        st = C.c_void_p(stream) if stream is not None else _stream()
+        out = (C.c_double * 4)()
+        check(lib().lp_engine_hbm_bench(self.handle, int(step), int(iters), int(sets), st, out))
+        return {"k1_ms": out[0], "k1_bytes": out[1], "k10_ms": out[2], "k10_bytes": out[3]}
+
     def step_phase(self, step, phase, stream=None):
         """lp_engine_step_phase: 1 = compute this rank's shards, 2 = NCCL exchange, 3 = reconstruct."""
         st = C.c_void_p(stream) if stream is not None else _stream()

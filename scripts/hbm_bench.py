@@ -1,6 +1,9 @@
 """K1 (partition gather) and K10 (reconstruct + sampler update) micro-benchmark at the BASELINE
-latent sizes: per-launch device time (CUDA events, L2 flushed before every launch so inputs
-come from HBM), achieved algorithmic GB/s and fraction of the measured HBM copy bandwidth.
+latent sizes: per-launch device time, achieved algorithmic GB/s and fraction of the measured HBM
+copy bandwidth.  Two timings per kernel: `*_us` = 64 back-to-back launches over 8 private
+buffer copies used round robin (working set > L2, launch overhead amortised; the bench.py
+method), and `*_flush_us` = one launch between L2 flushes, CUDA events around it (~2 us event
+granularity: an upper bound).
 
 Algorithmic bytes: K1 = 2 * shard elements * b; K10 = (sum of shard elements +
 2 * latent elements) * b (every prediction read once, z read and written).
@@ -39,22 +42,52 @@ def timed(fn, reps=20):
     return ts[len(ts) // 2]
 
 
+SETS, ITERS = 8, 64
+
+
+def replay(fn):
+    """Per-launch ms of ITERS back-to-back launches fn(i % SETS) (one event pair around all)."""
+    for i in range(SETS):
+        fn(i)
+    a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+    a.record()
+    for i in range(ITERS):
+        fn(i % SETS)
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / ITERS
+
+
 def case(name, dims, K, r, d):
     out = []
     n = 1
     for x in dims:
         n *= x
-    z = torch.randn(n, device="cuda").to(DT[d]) if d != 2 else torch.randint(0, 0x3b00, (n,), device="cuda", dtype=torch.int16)
+    zs = []
+    for _ in range(SETS):
+        zs.append(torch.randn(n, device="cuda").to(DT[d]) if d != 2 else
+                  torch.randint(0, 0x3b00, (n,), device="cuda", dtype=torch.int16))
+    z = zs[0]
     for step, axis in ((1, "T"), (2, "H"), (3, "W")):
         plan = lp.build_plan(dims, (1, 2, 2), step, K, r)
         subs = [plan.sub_shape(dims, k) for k in range(plan.workers)]
         vols = [s[0] * s[1] * s[2] * s[3] for s in subs]
-        packed = torch.empty(sum(vols), device="cuda", dtype=DT[d])
-        if d == 2:
-            packed.copy_(torch.randint(0, 0x3b00, (sum(vols),), device="cuda", dtype=torch.int16))
-        else:
-            packed.normal_()
+        packs = []
+        for _ in range(SETS):
+            packed = torch.empty(sum(vols), device="cuda", dtype=DT[d])
+            if d == 2:
+                packed.copy_(torch.randint(0, 0x3b00, (sum(vols),), device="cuda", dtype=torch.int16))
+            else:
+                packed.normal_()
+            packs.append(packed)
+        packed = packs[0]
         shape = _lib.i64arr(dims)
+        ex = lambda i: _lib.check(L.lp_extract(C.byref(plan.raw), 0, plan.workers, C.c_void_p(zs[i].data_ptr()),  # noqa: E731
+                                               shape, d, C.c_void_p(packs[i].data_ptr()), st()))
+        ru = lambda i, fast: _lib.check(L.lp_reconstruct_update(C.byref(plan.raw), C.c_void_p(packs[i].data_ptr()),  # noqa: E731
+                                                               shape, d, fast, C.c_double(1e-30),
+                                                               C.c_void_p(zs[i].data_ptr()), st()))
+        k1r, k10r, k10fr = replay(ex), replay(lambda i: ru(i, 0)), replay(lambda i: ru(i, 1))
         # K1: gather every entry (one launch for all entries, as the engine does for its owned run)
         k1 = timed(lambda: _lib.check(L.lp_extract(C.byref(plan.raw), 0, plan.workers, C.c_void_p(z.data_ptr()), shape, d,
                                                    C.c_void_p(packed.data_ptr()), st())))
@@ -65,9 +98,11 @@ def case(name, dims, K, r, d):
         k10f = timed(lambda: _lib.check(L.lp_reconstruct_update(C.byref(plan.raw), C.c_void_p(packed.data_ptr()), shape, d, 1,
                                                                C.c_double(1e-30), C.c_void_p(z.data_ptr()), st())))
         row = {"config": name, "axis": axis, "K": K, "dtype_bytes": d, "latent_elems": n, "shard_elems": sum(vols),
-               "k1_us": k1 * 1e3, "k1_GBps": k1_bytes / k1 / 1e6, "k1_frac": k1_bytes / k1 / 1e6 / PEAK,
-               "k10_us": k10 * 1e3, "k10_GBps": k10_bytes / k10 / 1e6, "k10_frac": k10_bytes / k10 / 1e6 / PEAK,
-               "k10_fast_us": k10f * 1e3, "k10_fast_frac": k10_bytes / k10f / 1e6 / PEAK}
+               "k1_us": k1r * 1e3, "k1_GBps": k1_bytes / k1r / 1e6, "k1_frac": k1_bytes / k1r / 1e6 / PEAK,
+               "k10_us": k10r * 1e3, "k10_GBps": k10_bytes / k10r / 1e6, "k10_frac": k10_bytes / k10r / 1e6 / PEAK,
+               "k10_fast_us": k10fr * 1e3, "k10_fast_frac": k10_bytes / k10fr / 1e6 / PEAK,
+               "k1_flush_us": k1 * 1e3, "k10_flush_us": k10 * 1e3, "k10_fast_flush_us": k10f * 1e3,
+               "k1_bytes": k1_bytes, "k10_bytes": k10_bytes}
         print(json.dumps(row), flush=True)
         out.append(row)
     return out

@@ -212,6 +212,9 @@ int lp_copy_to_device(void* dst, const void* src, size_t bytes);
 int lp_copy_to_host(void* dst, const void* src, size_t bytes);
 /* Kernel launches issued by this library since load. */
 uint64_t lp_launch_count(void);
+/* Frees the library's device-side caches (K10 coverage tables; rebuilt on next use).  Waits for
+ * the device.  The cache is also bounded (64 tables) and flushed when full. */
+int lp_release_caches(void);
 /* Live per-kernel-class timing with CUDA events on the launching stream
  * (classes: 0 self-attention, 1 cross-attention, 2 GEMM, 3 K9 all-gather, 4 K1 gather,
  * 5 K10 reconstruct+update).  collect() fills 6 entries each: launches, device ms,

@@ -102,6 +102,7 @@ _SIGS = {
     "lp_device_check": (_i, [_i]),
     "lp_device_flags": (_i, [C.POINTER(C.c_uint32), _i]),
     "lp_launch_count": (C.c_uint64, []),
+    "lp_release_caches": (_i, []),
     "lp_profile_enable": (_i, [_i]),
     "lp_tune": (_i, [C.c_char_p, _i]),
     "lp_profile_collect": (_i, [C.POINTER(C.c_uint64), _f64p, _f64p, _f64p]),

@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 
 #include "dit_kernels.hpp"
+#include "lnfold.cuh"
 
 namespace lpb200 {
 
@@ -225,6 +226,80 @@ void layernorm_bf16(const float* x, __nv_bfloat16* y, int64_t rows, int d, const
     LP_LN(1) LP_LN(2) LP_LN(4) LP_LN(8) LP_LN(12) LP_LN(16) LP_LN(24) LP_LN(32) LP_LN(40)
 #undef LP_LN
     fail(LP_ERR_INVALID_ARGUMENT, "layernorm: unsupported width");
+}
+
+// ---------------------------------------------------------------------------
+// LayerNorm fold: per-matrix column sums / folded biases (one warp per output row n)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_lnfold_vec(const LnFoldJob* __restrict__ jobs) {
+    const LnFoldJob j = jobs[blockIdx.y];
+    const int n = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x & 31;
+    if (n >= j.N) return;
+    const __nv_bfloat16* w = j.W + static_cast<int64_t>(n) * j.K;
+    float cs = 0.f, bo = 0.f;
+    for (int k = 8 * lane; k < j.K; k += 256) {
+        const uint4 u = *reinterpret_cast<const uint4*>(w + k);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+        const float4 a0 = *reinterpret_cast<const float4*>(j.a + k), a1 = *reinterpret_cast<const float4*>(j.a + k + 4);
+        const float4 b0 = *reinterpret_cast<const float4*>(j.b + k), b1 = *reinterpret_cast<const float4*>(j.b + k + 4);
+        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int u2 = 0; u2 < 4; ++u2) {
+            const float2 wf = __bfloat1622float2(h[u2]);
+            cs = fmaf(wf.x, j.plus1 ? 1.f + av[2 * u2] : av[2 * u2], cs);
+            cs = fmaf(wf.y, j.plus1 ? 1.f + av[2 * u2 + 1] : av[2 * u2 + 1], cs);
+            bo = fmaf(wf.x, bv[2 * u2], bo);
+            bo = fmaf(wf.y, bv[2 * u2 + 1], bo);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        cs += __shfl_xor_sync(0xffffffff, cs, o);
+        bo += __shfl_xor_sync(0xffffffff, bo, o);
+    }
+    if (lane == 0) {
+        j.cs[n] = cs;
+        j.bo[n] = bo + (j.bias ? j.bias[n] : 0.f);
+    }
+}
+
+void lnfold_vectors(const LnFoldJob* jobs_dev, int njobs, int max_n, cudaStream_t st) {
+    if (njobs <= 0) return;
+    k_lnfold_vec<<<dim3(static_cast<unsigned>((max_n + 7) / 8), static_cast<unsigned>(njobs)), 256, 0, st>>>(jobs_dev);
+    LP_LAUNCH_CHECK();
+}
+
+// One thread per (row, part): the part's columns in 32-value chunks, through the same
+// operations as the GEMM producer epilogue (lnfold.cuh), so the partials are bit-identical.
+__global__ void __launch_bounds__(256) k_ln_stats_xq(const float* __restrict__ x, __nv_bfloat16* __restrict__ xq,
+                                                     float2* __restrict__ stats, int64_t rows, int d,
+                                                     const float* __restrict__ g, int plus1, int parts) {
+    const int64_t i = blockIdx.x * 256LL + threadIdx.x;
+    if (i >= rows * parts) return;
+    const int64_t row = i / parts;
+    const int part = static_cast<int>(i - row * parts), w = d / parts;
+    float mean = 0.f, m2 = 0.f;
+    for (int c = 0; c < w / 32; ++c) {
+        const int col0 = part * w + 32 * c;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(v + j) = *reinterpret_cast<const float4*>(x + row * d + col0 + j);
+        ln_chunk_merge(v, c, mean, m2);
+        uint4* o = reinterpret_cast<uint4*>(xq + row * d + col0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = ln_xq8(v + 8 * j, g + col0 + 8 * j, plus1);
+    }
+    stats[i] = make_float2(mean, m2);
+}
+
+void ln_stats_xq(const float* x, __nv_bfloat16* xq, float2* stats, int64_t rows, int d, const float* g, bool plus1,
+                 int parts, cudaStream_t st) {
+    if (parts < 1 || d % parts || (d / parts) % 32) fail(LP_ERR_INVALID_ARGUMENT, "ln_stats_xq: parts must split d into 32-column chunks");
+    const int64_t n = rows * parts;
+    k_ln_stats_xq<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(x, xq, stats, rows, d, g, plus1 ? 1 : 0, parts);
+    LP_LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------------------------

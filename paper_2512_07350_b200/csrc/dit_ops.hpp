@@ -15,7 +15,28 @@ struct GemmEpilogue {
     void* out;          // bf16 / f32 [M, ldo]
     int64_t ldo;        // output row stride (elements)
     const float* gate;  // [N] or null (F32_RESID only)
+    // LayerNorm folded into the next GEMM (dit.cpp, knob dit_lnfold), producer side (F32 /
+    // F32_RESID): besides x the epilogue writes xq = bf16(x * g) (g_plus1: x * (1 + g); row
+    // stride ldq) — the next LayerNorm's per-channel multiplier applied — and, per row and
+    // N tile, the tile's LayerNorm partials (mean, M2 = sum (x - mean)^2) of x at
+    // stats_out[row * (N / BN) + n_tile].  Null xq: off.
+    __nv_bfloat16* xq;
+    int64_t ldq;
+    const float* g;
+    int g_plus1;
+    float2* stats_out;
+    // consumer side (BF16 / BF16_GELU with A = xq): out = rstd * (acc - mean * cs[col]) + bias[col]
+    // with (mean, rstd = 1/sqrt(var + eps)) merged from the row's `parts` partials of
+    // cols_per_part columns each (stats_in[row * parts ...]).  Null stats_in: off.
+    const float* cs;
+    const float2* stats_in;
+    int parts;
+    float cols_per_part;
+    float eps;
 };
+// N tile width the GEMM uses for N (the producer's partial count is N / gemm_bn_for(M, N));
+// 0 when (M, N) takes a kernel without the LN-fold epilogue.
+int gemm_lnfold_bn(int M, int N);
 
 // D = epilogue(A[M,K] · B[N,K]^T); lda/ldb in elements.
 void gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const GemmEpilogue& ep,

@@ -145,6 +145,7 @@ int lp_engine_create(const lp_engine_config* c, const uint8_t* nccl_id, const do
                                             c->assign == LP_ASSIGN_BALANCED ? &cost : nullptr);
                 e->elems[a] = entry_elems(e->plans[a], e->shape);
                 e->recon[a] = make_recon_params(e->plans[a], e->shape, e->layout[a].base, c->eta);
+                e->recon[a].table = recon_table_build(e->recon[a], nullptr);  // owned: graphs embed it
                 max_slot = std::max(max_slot, e->layout[a].slot_elems);
             }
             const size_t E = static_cast<size_t>(c->dtype_bytes);
@@ -227,6 +228,8 @@ int lp_engine_destroy(lp_engine* e) {
     }
     if (e->ev_fork) cudaEventDestroy(e->ev_fork);
     cudaFree(e->ws);
+    for (auto& r : e->recon)
+        if (r.table) cudaFree(const_cast<void*>(r.table));
     delete e;
     return LP_OK;
 }

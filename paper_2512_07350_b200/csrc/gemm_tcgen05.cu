@@ -22,6 +22,7 @@
 #include <mutex>
 
 #include "dit_ops.hpp"
+#include "lnfold.cuh"
 #include "tc_ptx.cuh"
 
 namespace lpb200 {
@@ -92,6 +93,22 @@ CUtensorMap make_tmap_3d_bf16(const void* base, uint64_t d0, uint64_t d1, uint64
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(LP_ERR_CUDA, "cuTensorMapEncodeTiled(3d) failed: " + std::to_string(r));
     return m;
+}
+
+// Plain 2-D map of 2/4/8-byte elements (no swizzle, zero OOB fill): K1's TMA-staged gather.
+// Returns false when the driver rejects the geometry (stride or box not 16-B multiples).
+bool make_tmap_2d_raw(CUtensorMap* m, const void* base, int elem_bytes, uint64_t inner, uint64_t outer,
+                      uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+    const cuuint64_t dims[2] = {inner, outer};
+    const cuuint64_t strides[1] = {row_stride_bytes};
+    const cuuint32_t box[2] = {box_inner, box_outer};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapDataType dt = elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                   : elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
+                                                     : CU_TENSOR_MAP_DATA_TYPE_INT64;
+    return encode_fn()(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // ---------------------------------------------------------------------------
@@ -289,17 +306,35 @@ __device__ __forceinline__ void tma_load_2d_cta(const void* tmap, uint64_t* bar,
         : "memory");
 }
 
+// Per-row LayerNorm state of the LN-fold epilogue (one lane = one row of the tile).
+struct LnRow {
+    float mean = 0.f, rstd = 1.f;  // consumer: the row's LayerNorm statistics
+    float st_mean = 0.f, st_m2 = 0.f;  // producer: running partials over this tile's chunks
+    __nv_bfloat16* xq = nullptr;  // producer: this row's xq (null: row >= M or off)
+};
+
 template <int MODE>
-__device__ __forceinline__ void epi_chunk_smem(const GemmEpilogue& ep, int col0, const uint32_t (&r)[32], uint8_t* box) {
+__device__ __forceinline__ void epi_chunk_smem(const GemmEpilogue& ep, int col0, const uint32_t (&r)[32], uint8_t* box,
+                                               LnRow& ln, int chunk) {
     const uint32_t lane = lane_id();
     float v[32];
 #pragma unroll
     for (int j = 0; j < 32; j += 4) {
         const float4 b = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        v[j] = __uint_as_float(r[j]) + b.x;
-        v[j + 1] = __uint_as_float(r[j + 1]) + b.y;
-        v[j + 2] = __uint_as_float(r[j + 2]) + b.z;
-        v[j + 3] = __uint_as_float(r[j + 3]) + b.w;
+        float a0 = __uint_as_float(r[j]), a1 = __uint_as_float(r[j + 1]), a2 = __uint_as_float(r[j + 2]),
+              a3 = __uint_as_float(r[j + 3]);
+        if ((MODE == EPI_BF16 || MODE == EPI_BF16_GELU) && ep.stats_in) {
+            // LN folded into this GEMM: A was bf16(x * g), so acc - mean * cs = sum_k (x_k - mean) g_k W_nk
+            const float4 c = __ldg(reinterpret_cast<const float4*>(ep.cs + col0 + j));
+            a0 = ln.rstd * fmaf(-ln.mean, c.x, a0);
+            a1 = ln.rstd * fmaf(-ln.mean, c.y, a1);
+            a2 = ln.rstd * fmaf(-ln.mean, c.z, a2);
+            a3 = ln.rstd * fmaf(-ln.mean, c.w, a3);
+        }
+        v[j] = a0 + b.x;
+        v[j + 1] = a1 + b.y;
+        v[j + 2] = a2 + b.z;
+        v[j + 3] = a3 + b.w;
     }
     if (MODE == EPI_BF16 || MODE == EPI_BF16_GELU) {
         uint8_t* row = box + lane * 64;
@@ -329,6 +364,24 @@ __device__ __forceinline__ void epi_chunk_smem(const GemmEpilogue& ep, int col0,
                 x = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             }
             *p = x;
+            v[4 * j] = x.x;  // v now holds the chunk's x (LN-fold producer below)
+            v[4 * j + 1] = x.y;
+            v[4 * j + 2] = x.z;
+            v[4 * j + 3] = x.w;
+        }
+        if (ep.xq) {
+            // LayerNorm partials of this chunk's 32 values, merged into the tile's (lnfold.cuh)
+            ln_chunk_merge(v, chunk, ln.st_mean, ln.st_m2);
+            if (ln.xq) {
+                uint4* o = reinterpret_cast<uint4*>(ln.xq + col0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    float g[8];
+                    *reinterpret_cast<float4*>(g) = __ldg(reinterpret_cast<const float4*>(ep.g + col0 + 8 * j));
+                    *reinterpret_cast<float4*>(g + 4) = __ldg(reinterpret_cast<const float4*>(ep.g + col0 + 8 * j + 4));
+                    o[j] = ln_xq8(v + 8 * j, g, ep.g_plus1);
+                }
+            }
         }
     }
 }
@@ -494,6 +547,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             tc_fence_after();
             const int row0 = mb * 2 * kBM + rank * kBM + q * 32;
             const uint32_t taddr = tmem + ((q * 32) << 16) + acc * BN;
+            const int my_row = row0 + static_cast<int>(lane);
+            LnRow ln;
+            if ((MODE == EPI_BF16 || MODE == EPI_BF16_GELU) && ep.stats_in && my_row < M) {
+                // the row's LayerNorm statistics from its producer partials (equal counts)
+                const float2* sp = ep.stats_in + static_cast<int64_t>(my_row) * ep.parts;
+                float ms = 0.f;
+                for (int i = 0; i < ep.parts; ++i) ms += sp[i].x;
+                const float mean = ms / static_cast<float>(ep.parts);
+                float m2 = 0.f;
+                for (int i = 0; i < ep.parts; ++i) {
+                    const float2 pi = sp[i];
+                    const float dlt = pi.x - mean;
+                    m2 += pi.y + ep.cols_per_part * dlt * dlt;
+                }
+                ln.mean = mean;
+                ln.rstd = rsqrtf(m2 / (ep.cols_per_part * static_cast<float>(ep.parts)) + ep.eps);
+            }
+            if (MODE >= EPI_F32_RESID && ep.xq && my_row < M) ln.xq = ep.xq + static_cast<int64_t>(my_row) * ep.ldq;
 #pragma unroll 1
             for (int c = 0; c < NCH; ++c, ++u) {
                 const int b = u % NB;
@@ -508,7 +579,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 }
                 __syncwarp();
                 tmem_ld_wait();
-                epi_chunk_smem<MODE>(ep, nb * BN + c * 32, r, boxes + b * kEpiBox);
+                epi_chunk_smem<MODE>(ep, nb * BN + c * 32, r, boxes + b * kEpiBox, ln, c);
                 fence_proxy_async();
                 __syncwarp();
                 if (lane == 0) {
@@ -516,6 +587,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                     bulk_commit();
                 }
             }
+            if (MODE >= EPI_F32_RESID && ep.stats_out && my_row < M)
+                ep.stats_out[static_cast<int64_t>(my_row) * num_n + nb] = make_float2(ln.st_mean, ln.st_m2);
             tc_fence_before();
             mbar_arrive_cluster(&tempty[acc], 0);
         }
@@ -622,9 +695,20 @@ static void gemm_bn(const CUtensorMap& ta, const void* B, int64_t ldb, const Gem
     }
 }
 
+int gemm_lnfold_bn(int M, int N) {
+    if (!kEpiTma || !gemm_variant() || M <= kBM) return 0;
+    return N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 0);
+}
+
 void gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const GemmEpilogue& ep,
                int mode, cudaStream_t st) {
     if (M <= 0) return;
+    if ((ep.xq || ep.stats_in) && !gemm_lnfold_bn(M, N))
+        fail(LP_ERR_INVALID_ARGUMENT, "gemm: the LN-fold epilogue needs the CTA-pair kernel (M > 128, N % 128 == 0)");
+    if (ep.xq && (mode < EPI_F32_RESID || !ep.g || !ep.stats_out || ep.ldq % 8))
+        fail(LP_ERR_INVALID_ARGUMENT, "gemm: LN-fold producer needs an f32 epilogue, g, stats_out and ldq % 8 == 0");
+    if (ep.stats_in && (mode > EPI_BF16_GELU || !ep.cs || ep.parts < 1))
+        fail(LP_ERR_INVALID_ARGUMENT, "gemm: LN-fold consumer needs a bf16 epilogue, cs and parts >= 1");
     if (K % 8 || lda % 8 || ldb % 8) fail(LP_ERR_INVALID_ARGUMENT, "gemm: K and strides must be multiples of 8");
     const CUtensorMap ta = make_tmap_2d_bf16(A, K, M, lda * 2, kBK, kBM);
     prof_begin(KC_GEMM, st);

@@ -98,6 +98,10 @@ __global__ void __launch_bounds__(256) k_slice_copy32(const V* __restrict__ src,
 // warp's lane 0 is an independent copy engine with two shared-memory stages: bulk-load a
 // chunk (mbarrier complete_tx), bulk-store it, and load the next chunk into the other
 // stage while the store drains.  Requires 16-byte alignment of addresses, run and stride.
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
+    return static_cast<uint32_t>((static_cast<uint64_t>(x) * f.mul) >> f.shift);
+}
+
 constexpr int kSliceChunk = 16 * 1024, kSliceWarps = 4;
 __global__ void __launch_bounds__(32 * kSliceWarps) k_slice_bulk(const uint8_t* __restrict__ src,
                                                                  uint8_t* __restrict__ dst, int64_t outer,
@@ -170,6 +174,264 @@ __global__ void __launch_bounds__(256) k_gather_entries(const __grid_constant__ 
     }
 }
 
+// K1, TMA-staged form (the default where its alignment conditions hold; knob gather_tma=0
+// falls back to the vector-copy kernel above).
+//  * W-axis windows (inner == 1: every latent row (c, t, h) contributes one short run of len
+//    elements): one 2-D tensor map per entry over z viewed as [rows = C*T*H][W] with box
+//    {lb, R} (lb = len rounded up to a 16-byte multiple).  Each CTA pulls R-row boxes through a
+//    kGtStages-deep shared-memory ring (one thread issues cp.async.bulk.tensor, completion on an
+//    mbarrier); R consecutive rows of one entry are ONE contiguous span of R*len elements in dst,
+//    which the block writes out as 16-byte vectors (coalesced, no strided global access at all).
+//  * T/H windows (inner > 1: each row contributes a contiguous run of len*inner elements):
+//    1-D bulk copies through shared memory (TMA engine, no thread touches the data), all
+//    entries in one launch.
+constexpr int kGtMaxEntries = 8, kGtStages = 4, kGtThreads = 256;
+struct GatherTmaEntry {
+    uint32_t len, lb, s, items_begin;
+    uint64_t dst_off;  // elements
+    FastDiv div_len;
+};
+struct GatherTmaParams {
+    int n;
+    uint32_t rows, R, items, stage_bytes;
+    GatherTmaEntry e[kGtMaxEntries];
+};
+struct GatherTmaMaps {
+    CUtensorMap m[kGtMaxEntries];
+};
+template <int E> struct ElemOf;
+template <> struct ElemOf<2> { using T = uint16_t; };
+template <> struct ElemOf<4> { using T = uint32_t; };
+template <> struct ElemOf<8> { using T = unsigned long long; };
+
+template <int E>
+__global__ void __launch_bounds__(kGtThreads) k_gather_tma(const __grid_constant__ GatherTmaMaps maps,
+                                                           const __grid_constant__ GatherTmaParams p,
+                                                           typename ElemOf<E>::T* __restrict__ dst) {
+    using T = typename ElemOf<E>::T;
+    constexpr int V = 16 / E;  // elements per 16-byte vector
+    extern __shared__ __align__(128) uint8_t sbuf[];
+    __shared__ uint64_t full[kGtStages];
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < kGtStages; ++s) tc::mbar_init(&full[s], 1);
+        tc::fence_barrier_init();
+    }
+    __syncthreads();
+    auto locate = [&](uint32_t it, int& k, uint32_t& row0) {
+        k = 0;
+        while (k + 1 < p.n && it >= p.e[k + 1].items_begin) ++k;
+        row0 = (it - p.e[k].items_begin) * p.R;
+    };
+    auto issue = [&](uint32_t it, int s) {
+        int k;
+        uint32_t row0;
+        locate(it, k, row0);
+        // the transaction counts the whole box, rows past the tensor end included (zero-filled)
+        tc::mbar_arrive_expect_tx(&full[s], p.e[k].lb * p.R * E);
+        tc::tma_load_2d(&maps.m[k], &full[s], sbuf + s * p.stage_bytes, static_cast<int32_t>(p.e[k].s),
+                        static_cast<int32_t>(row0));
+    };
+    const uint32_t first = blockIdx.x, step = gridDim.x;
+    const uint32_t n_my = first < p.items ? (p.items - first + step - 1) / step : 0;
+    if (tid == 0)
+        for (uint32_t j = 0; j < n_my && j < kGtStages; ++j) issue(first + j * step, static_cast<int>(j));
+    for (uint32_t j = 0; j < n_my; ++j) {
+        const int s = static_cast<int>(j % kGtStages);
+        int k;
+        uint32_t row0;
+        locate(first + j * step, k, row0);
+        const GatherTmaEntry& e = p.e[k];
+        const uint32_t span = min(p.R, p.rows - row0) * e.len;
+        const T* box = reinterpret_cast<const T*>(sbuf + s * p.stage_bytes);
+        T* out = dst + e.dst_off + static_cast<uint64_t>(row0) * e.len;
+        tc::mbar_wait(&full[s], (j / kGtStages) & 1u);
+        const uint32_t nv = span / V;
+        for (uint32_t v = tid; v < nv; v += kGtThreads) {
+            T tmp[V];
+#pragma unroll
+            for (int u = 0; u < V; ++u) {
+                const uint32_t idx = v * V + u;
+                const uint32_t r = fdiv(idx, e.div_len);
+                tmp[u] = box[r * e.lb + (idx - r * e.len)];
+            }
+            *reinterpret_cast<uint4*>(out + v * V) = *reinterpret_cast<const uint4*>(tmp);
+        }
+        for (uint32_t idx = nv * V + tid; idx < span; idx += kGtThreads) {
+            const uint32_t r = fdiv(idx, e.div_len);
+            out[idx] = box[r * e.lb + (idx - r * e.len)];
+        }
+        __syncthreads();  // stage s has been read by every thread
+        if (tid == 0 && j + kGtStages < n_my) issue(first + (j + kGtStages) * step, s);
+    }
+}
+
+// T/H windows: every entry's rows are runs of run_b contiguous bytes (src stride stride_b),
+// cut into <= kSliceChunk pieces; a warp's lane 0 is a copy engine with two stages (bulk load
+// -> mbarrier -> bulk store), chunks dealt round robin over all warps of the grid.
+struct GatherBulkEntry {
+    uint64_t run_b, off_b, dst_b, chunks_begin, cpr;
+};
+struct GatherBulkParams {
+    int n;
+    uint64_t stride_b, chunks;
+    GatherBulkEntry e[kGtMaxEntries];
+};
+__global__ void __launch_bounds__(32 * kSliceWarps) k_gather_bulk(const __grid_constant__ GatherBulkParams p,
+                                                                  const uint8_t* __restrict__ src,
+                                                                  uint8_t* __restrict__ dst) {
+    extern __shared__ __align__(128) uint8_t sbuf[];  // [warps][2][chunk]
+    __shared__ uint64_t bars[kSliceWarps][2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane != 0) return;
+    uint64_t* bar = bars[warp];
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::fence_barrier_init();
+    uint8_t* buf = sbuf + static_cast<size_t>(warp) * 2 * kSliceChunk;
+    const uint64_t engines = static_cast<uint64_t>(gridDim.x) * kSliceWarps;
+    uint32_t ph[2] = {0, 0};
+    int it = 0;
+    for (uint64_t c = static_cast<uint64_t>(blockIdx.x) * kSliceWarps + warp; c < p.chunks; c += engines, ++it) {
+        int k = 0;
+        while (k + 1 < p.n && c >= p.e[k + 1].chunks_begin) ++k;
+        const GatherBulkEntry& e = p.e[k];
+        const uint64_t r = c - e.chunks_begin, o = r / e.cpr, at = (r - o * e.cpr) * kSliceChunk;
+        const uint32_t bytes = static_cast<uint32_t>(min(static_cast<uint64_t>(kSliceChunk), e.run_b - at));
+        const int b = it & 1;
+        if (it >= 2) tc::bulk_wait_read<1>();  // the store issued from this stage two chunks ago has read it
+        tc::mbar_arrive_expect_tx(&bar[b], bytes);
+        tc::bulk_load(buf + b * kSliceChunk, src + o * p.stride_b + e.off_b + at, bytes, &bar[b]);
+        tc::mbar_wait(&bar[b], ph[b]);
+        ph[b] ^= 1;
+        tc::bulk_store(dst + e.dst_b + o * e.run_b + at, buf + b * kSliceChunk, bytes);
+        tc::bulk_commit();
+    }
+    tc::bulk_wait_all();
+}
+
+bool make_tmap_2d_raw(CUtensorMap* m, const void* base, int elem_bytes, uint64_t inner, uint64_t outer,
+                      uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);  // gemm_tcgen05.cu
+
+static int num_sms_lp() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+// The TMA-staged K1 of entries ks[0..count) (packed in that order); false when its alignment
+// conditions do not hold (the caller then uses the vector-copy kernel).
+static bool gather_tma(const void* z, const Shape4& s, const lp_plan& plan, const int* ks, int count, int E, void* dst,
+                       cudaStream_t st) {
+    if (count <= 0 || count > kGtMaxEntries || !tune_get("gather_tma", 1)) return false;
+    i64 outer, inner;
+    axis_view(s, plan.axis, outer, inner);
+    const i64 D = s.extent(plan.axis);
+    if (reinterpret_cast<uintptr_t>(z) % 16 || reinterpret_cast<uintptr_t>(dst) % 16) return false;
+    if (inner > 1) {
+        GatherBulkParams p;
+        std::memset(&p, 0, sizeof(p));
+        p.n = count;
+        p.stride_b = static_cast<uint64_t>(D * inner * E);
+        if (p.stride_b % 16) return false;
+        uint64_t chunks = 0, dst_b = 0;
+        for (int c = 0; c < count; ++c) {
+            const lp_entry& en = plan.entries[ks[c]];
+            GatherBulkEntry& g = p.e[c];
+            g.run_b = static_cast<uint64_t>((en.latent_end - en.latent_begin) * inner * E);
+            g.off_b = static_cast<uint64_t>(en.latent_begin * inner * E);
+            g.dst_b = dst_b;
+            if (g.run_b % 16 || g.off_b % 16 || g.dst_b % 16) return false;
+            g.cpr = (g.run_b + kSliceChunk - 1) / kSliceChunk;
+            g.chunks_begin = chunks;
+            chunks += g.cpr * static_cast<uint64_t>(outer);
+            dst_b += g.run_b * static_cast<uint64_t>(outer);
+        }
+        p.chunks = chunks;
+        static bool attr = false;
+        constexpr int smem = kSliceWarps * 2 * kSliceChunk;
+        if (!attr) {
+            LP_CUDA(cudaFuncSetAttribute(k_gather_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            attr = true;
+        }
+        const uint64_t want = (chunks + kSliceWarps - 1) / kSliceWarps;
+        const int grid = static_cast<int>(std::min<uint64_t>(want, 3ull * num_sms_lp()));
+        prof_begin(KC_GATHER, st);
+        k_gather_bulk<<<grid, 32 * kSliceWarps, smem, st>>>(p, static_cast<const uint8_t*>(z), static_cast<uint8_t*>(dst));
+        LP_LAUNCH_CHECK();
+        prof_end(KC_GATHER, st, 0.0, 2.0 * static_cast<double>(dst_b));
+        return true;
+    }
+    // inner == 1: W-axis boxes
+    const int V = 16 / E;
+    const uint64_t rows = static_cast<uint64_t>(outer);
+    if (rows >= (1ull << 31) || (D * E) % 16) return false;
+    uint32_t lbmax = 0;
+    for (int c = 0; c < count; ++c) {
+        const lp_entry& en = plan.entries[ks[c]];
+        const uint32_t len = static_cast<uint32_t>(en.latent_end - en.latent_begin);
+        const uint32_t lb = (len * E + 15) / 16 * 16 / E;
+        if (lb > 256) return false;
+        lbmax = std::max(lbmax, lb);
+    }
+    // R rows per box: ~16 KB stages, a multiple of V (so every box's span starts 16-B aligned)
+    uint32_t R = std::min<uint32_t>(256, 16384u / (lbmax * E));
+    R = R / V * V;
+    if (R < static_cast<uint32_t>(V)) return false;
+    GatherTmaParams p;
+    std::memset(&p, 0, sizeof(p));
+    GatherTmaMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    p.n = count;
+    p.rows = static_cast<uint32_t>(rows);
+    p.R = R;
+    p.stage_bytes = (lbmax * R * E + 127) / 128 * 128;
+    uint64_t off = 0;
+    uint32_t items = 0;
+    for (int c = 0; c < count; ++c) {
+        const lp_entry& en = plan.entries[ks[c]];
+        GatherTmaEntry& g = p.e[c];
+        g.len = static_cast<uint32_t>(en.latent_end - en.latent_begin);
+        g.lb = (g.len * E + 15) / 16 * 16 / E;
+        g.s = static_cast<uint32_t>(en.latent_begin);
+        g.items_begin = items;
+        g.dst_off = off;
+        g.div_len = make_fastdiv(g.len);
+        if (off % V) return false;
+        if (!make_tmap_2d_raw(&maps.m[c], z, E, static_cast<uint64_t>(D), rows, static_cast<uint64_t>(D * E), g.lb, R))
+            return false;
+        items += static_cast<uint32_t>((rows + R - 1) / R);
+        off += rows * g.len;
+    }
+    p.items = items;
+    const int smem = kGtStages * static_cast<int>(p.stage_bytes);
+    static int attr_bytes[9] = {};
+    if (attr_bytes[E] < smem) {
+        switch (E) {
+            case 2: LP_CUDA(cudaFuncSetAttribute(k_gather_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); break;
+            case 4: LP_CUDA(cudaFuncSetAttribute(k_gather_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); break;
+            default: LP_CUDA(cudaFuncSetAttribute(k_gather_tma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); break;
+        }
+        attr_bytes[E] = smem;
+    }
+    const int per_sm = std::max(1, std::min(4, (200 * 1024) / smem));
+    const int grid = static_cast<int>(std::min<uint64_t>(items, static_cast<uint64_t>(per_sm) * num_sms_lp()));
+    prof_begin(KC_GATHER, st);
+    switch (E) {
+        case 2: k_gather_tma<2><<<grid, kGtThreads, smem, st>>>(maps, p, static_cast<uint16_t*>(dst)); break;
+        case 4: k_gather_tma<4><<<grid, kGtThreads, smem, st>>>(maps, p, static_cast<uint32_t*>(dst)); break;
+        default: k_gather_tma<8><<<grid, kGtThreads, smem, st>>>(maps, p, static_cast<unsigned long long*>(dst)); break;
+    }
+    LP_LAUNCH_CHECK();
+    prof_end(KC_GATHER, st, 0.0, 2.0 * static_cast<double>(off) * E);
+    return true;
+}
+
 // Builds the one-launch gather of entries ks[0..count) of `plan` (packed in that order);
 // false when 32-bit vector indexing does not fit (the caller then copies entry by entry).
 static bool gather_params(const void* z, const Shape4& s, const lp_plan& plan, const int* ks, int count, int E,
@@ -205,6 +467,7 @@ static bool gather_params(const void* z, const Shape4& s, const lp_plan& plan, c
 
 void gather_entries(const void* z, const Shape4& s, const lp_plan& plan, const int* ks, int count, int E, void* dst,
                     cudaStream_t st) {
+    if (gather_tma(z, s, plan, ks, count, E, dst, st)) return;
     i64 outer, inner;
     axis_view(s, plan.axis, outer, inner);
     GatherParams p;
@@ -546,9 +809,6 @@ __global__ void __launch_bounds__(256) k_reconstruct(const __grid_constant__ Rec
     }
 }
 
-__device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
-    return static_cast<uint32_t>((static_cast<uint64_t>(x) * f.mul) >> f.shift);
-}
 
 // K10, exact mode, 32-bit indexing: the per-position weights w_k(x) and their sum
 // Z(x) = Σ_k w_k(x) (worker order, the same IEEE divisions and adds as entry_weight and
@@ -897,10 +1157,21 @@ static size_t recon_cov_bytes(const ReconParams& p, int dtype) {
 }
 
 // Device coverage tables, cached per (device, plan entries, gather bases, D, inner).  Built on
-// first use (eagerly: the engine's first step of an axis precedes any graph capture).
+// first use (eagerly: the engine's first step of an axis precedes any graph capture).  The
+// cache holds at most kReconTables tables; past that, or on lp_release_caches(), every table is
+// freed (cudaFree waits for the device, so no in-flight K10 still reads one).
+constexpr size_t kReconTables = 64;
+static std::mutex g_table_mu;
+static std::map<std::string, void*> g_tables;
+
+static void release_tables_locked() {
+    for (auto& kv : g_tables) cudaFree(kv.second);
+    g_tables.clear();
+}
+
 static const void* recon_table(const ReconParams& p, size_t bytes, cudaStream_t st) {
-    static std::mutex mu;
-    static std::map<std::string, void*> cache;
+    std::mutex& mu = g_table_mu;
+    std::map<std::string, void*>& cache = g_tables;
     int dev = 0;
     LP_CUDA(cudaGetDevice(&dev));
     std::string key(reinterpret_cast<const char*>(&dev), sizeof(dev));
@@ -914,6 +1185,7 @@ static const void* recon_table(const ReconParams& p, size_t bytes, cudaStream_t 
     LP_CUDA(cudaStreamIsCapturing(st, &cs));
     if (cs != cudaStreamCaptureStatusNone)
         fail(LP_ERR_INVALID_ARGUMENT, "K10 coverage table must be built by an eager launch before graph capture");
+    if (cache.size() >= kReconTables) release_tables_locked();
     void* t = nullptr;
     LP_CUDA(cudaMalloc(&t, bytes));
     k_recon_table<<<1, 256, 0, st>>>(p, t);
@@ -921,6 +1193,17 @@ static const void* recon_table(const ReconParams& p, size_t bytes, cudaStream_t 
     // published only once built: a caller on another stream may use it right away
     LP_CUDA(cudaStreamSynchronize(st));
     cache.emplace(std::move(key), t);
+    return t;
+}
+
+void* recon_table_build(const ReconParams& p, cudaStream_t st) {
+    const size_t bytes = recon_cov_bytes(p, 0);
+    if (!bytes) return nullptr;
+    void* t = nullptr;
+    LP_CUDA(cudaMalloc(&t, bytes));
+    k_recon_table<<<1, 256, 0, st>>>(p, t);
+    LP_LAUNCH_CHECK();
+    LP_CUDA(cudaStreamSynchronize(st));
     return t;
 }
 
@@ -935,7 +1218,7 @@ static void launch_recon(const ReconParams& p, const void* preds, void* z, void*
         bool vec = p.inner % 8 == 0 && al % (4 * D) == 0;  // 8 elements share (o, x); prediction vectors need 8-aligned bases
         for (int k = 0; k < p.n; ++k) vec = vec && p.e[k].base % 8 == 0;
         // one wave of resident blocks: each block builds its table once
-        const void* table = recon_table(p, cov, st);
+        const void* table = p.table ? p.table : recon_table(p, cov, st);
         const uint32_t tv = static_cast<uint32_t>(cov / 16);
         int res = 0;
         auto kfn = fast ? (vec ? k_reconstruct_cov<D, UPDATE, true, true> : k_reconstruct_cov<D, UPDATE, true, false>)
@@ -1102,6 +1385,13 @@ int lp_device_flags(uint32_t* flags_out, int reset) {
 
 uint64_t lp_launch_count(void) { return launch_count(); }
 
+int lp_release_caches(void) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lock(g_table_mu);
+        release_tables_locked();
+    });
+}
+
 // Device memory plumbing for hosts that bind only this header (the reference-side shim in
 // integration/): no cuda_runtime.h needed on the caller's side.
 int lp_device_alloc(size_t bytes, void** out) {
@@ -1148,7 +1438,21 @@ int lp_toy_predict(int32_t kind, const int64_t radius[3], double t_coeff, double
         check_dtype(dtype);
         const Shape4 s = Shape4::from(shape);
         double* ws = nullptr;
-        if (kind == LP_TOY_GLOBAL) LP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), s.c * sizeof(double), as_stream(stream)));
+        if (kind == LP_TOY_GLOBAL) {
+            // C doubles of per-channel means: stream-ordered from the device's default pool, which
+            // keeps freed blocks (release threshold raised once), so after the first call this is
+            // a pool hit — no cudaMalloc, no device synchronisation
+            static std::once_flag pool_once;
+            std::call_once(pool_once, [] {
+                int dev = 0;
+                cudaMemPool_t pool = nullptr;
+                if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                    uint64_t keep = UINT64_MAX;
+                    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+                }
+            });
+            LP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), s.c * sizeof(double), as_stream(stream)));
+        }
         toy_dispatch(kind, radius, z, s, dtype, toy_affine(t_coeff, timestep, cond_coeff, cond_mean), 0.0, 0.0, false,
                      out, ws, as_stream(stream));
         if (ws) LP_CUDA(cudaFreeAsync(ws, as_stream(stream)));

@@ -30,8 +30,14 @@ struct ReconParams {
     // peer exchange: the engine's failure word (non-zero = a peer's shard never arrived);
     // K10 then leaves z untouched instead of blending stale shards.  nullptr = no check.
     const unsigned* abort;
+    // K10 coverage table owned by the caller (an engine builds one per axis with
+    // recon_table_build and frees it at destroy); nullptr = the library's bounded cache
+    const void* table;
     ReconEntry e[kMaxKernelEntries];
 };
+// The coverage table of p as an owned device allocation (cudaFree it), or nullptr when K10's
+// coverage-table form does not apply to p.  Synchronizes `st`.
+void* recon_table_build(const ReconParams& p, cudaStream_t st);
 
 ReconParams make_recon_params(const lp_plan& plan, const Shape4& s, const std::vector<i64>& base, double eta);
 void reconstruct_dispatch(const ReconParams& p, int dtype, const void* preds, void* z, void* eps, bool update,

@@ -108,8 +108,27 @@ def case(name, dims, K, r, d):
     return out
 
 
+def ncu_pass(d):
+    """HB_NCU=1: each kernel once per C2 axis (K1, K10 exact, K10 fast), for ncu --set full."""
+    dims, n = (16, 21, 60, 104), 16 * 21 * 60 * 104
+    z = torch.randn(n, device="cuda").to(DT[d])
+    shape = _lib.i64arr(dims)
+    for step in (1, 2, 3):
+        plan = lp.build_plan(dims, (1, 2, 2), step, 4, 0.5)
+        vols = [s[0] * s[1] * s[2] * s[3] for s in (plan.sub_shape(dims, k) for k in range(plan.workers))]
+        packed = torch.randn(sum(vols), device="cuda").to(DT[d])
+        _lib.check(L.lp_extract(C.byref(plan.raw), 0, plan.workers, C.c_void_p(z.data_ptr()), shape, d,
+                                C.c_void_p(packed.data_ptr()), st()))
+        for fast in (0, 1):
+            _lib.check(L.lp_reconstruct_update(C.byref(plan.raw), C.c_void_p(packed.data_ptr()), shape, d, fast,
+                                               C.c_double(1e-30), C.c_void_p(z.data_ptr()), st()))
+    torch.cuda.synchronize()
+
+
 def main():
     d = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+    if os.environ.get("HB_NCU") == "1":
+        return ncu_pass(d)
     rows = []
     rows += case("C2", (16, 21, 60, 104), 4, 0.5, d)
     rows += case("C4", (16, 21, 90, 160), 8, 0.5, d)

@@ -185,6 +185,30 @@ def test_dit_single_pass_predict_vs_oracle(cuda):
         assert np.isfinite(rel) and rel <= 5e-2, (b, rel)
 
 
+@pytest.mark.parametrize("shape,t", [((16, 5, 16, 16), 37), ((16, 9, 30, 52), 4)])
+def test_lnfold_matches_layernorm_path_and_oracle(cuda, shape, t):
+    """The LayerNorm fold (knob dit_lnfold: LN partials + xq = bf16(x * g) written by the residual
+    GEMM epilogues, rstd * (acc - mean * cs) + b' in the next GEMM's epilogue) against the
+    separate-LayerNorm path and the fp32 oracle.  Both paths round differently (xq vs the
+    normalised h), so the bound is bf16-level, not bitwise."""
+    from tests.dit_reference import DiTReference
+
+    z, cond = lp.synthetic_latent(shape, 4, 2025)
+    dit = lp.DiTDenoiser(cond, num_layers=2)
+    outs = {}
+    for on in (0, 1):
+        _lib.check(_lib.lib().lp_tune(b"dit_lnfold", on))
+        outs[on] = dit.cfg_predict(z, t, 5.0).data.float().clone()
+    _lib.check(_lib.lib().lp_tune(b"dit_lnfold", 1))
+    rel = ((outs[1] - outs[0]).norm() / outs[0].norm()).item()
+    assert np.isfinite(rel) and rel <= 2e-2, rel
+    od, ck, cv = _oracle_ctx(dit, cond)
+    want, _ = DiTReference(od).forward(z.data.float(), t, ck, cv, 5.0)
+    for on in (0, 1):
+        r = ((outs[on] - want).norm() / want.norm()).item()
+        assert r <= 5e-2, (on, r)
+
+
 def test_block0_self_attention_dedupe_is_bit_identical(cuda):
     """Block 0's self-attention sub-block runs once for the two identical CFG halves (knob
     dit_dedupe0); the result equals the duplicated computation bit for bit."""

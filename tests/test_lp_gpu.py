@@ -41,6 +41,44 @@ def test_extract_bitexact(cuda, oracle):
         assert np.array_equal(got, want), (shape, patch, k, r, step, d)
 
 
+@pytest.mark.parametrize("d", [2, 4, 8])
+@pytest.mark.parametrize("dims,k,r", [((16, 21, 60, 104), 4, 0.5), ((3, 7, 12, 40), 3, 1.0), ((2, 5, 9, 24), 8, 0.25),
+                                      ((16, 41, 60, 104), 8, 0.5)])
+def test_extract_tma_paths_bitexact(cuda, oracle, d, dims, k, r):
+    """K1's TMA-staged forms (W axis: tensor-map boxes of R rows, repacked from shared memory;
+    T/H axes: 1-D bulk copies) against the oracle and against the vector-copy kernel
+    (knob gather_tma=0), all entries in one launch, on shapes whose geometry admits them."""
+    from paper_2512_07350_b200 import _lib
+
+    import ctypes as C
+
+    import torch
+
+    z, _ = oracle.synthetic(dims, d, 7)
+    zt = lp.LatentTensor.from_numpy(z, d)
+    L = _lib.lib()
+
+    def packed(plan):  # every entry in ONE launch (the engine's K1), packed in entry order
+        n = sum(int(np.prod(plan.sub_shape(dims, e))) for e in range(plan.workers))
+        out = lp.LatentTensor(torch.empty(n, dtype=zt.data.dtype, device="cuda"), d)
+        _lib.check(L.lp_extract(C.byref(plan.raw), 0, plan.workers, zt.ptr(), _lib.i64arr(dims), d, out.ptr(),
+                                C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return out.to_numpy()
+
+    for step in (1, 2, 3):
+        plan = lp.build_plan(dims, (1, 2, 2), step, k, r)
+        want = oracle.extract(z, oracle.build_plan(dims, (1, 2, 2), step, k, r))
+        assert np.array_equal(packed(plan), want), (dims, step, d)
+        one = np.concatenate([s.to_numpy().reshape(-1) for s in lp.extract_sublatents(zt, plan)])
+        assert np.array_equal(one, want), (dims, step, d)
+        _lib.check(L.lp_tune(b"gather_tma", 0))
+        try:
+            ref = packed(plan)
+        finally:
+            _lib.check(L.lp_tune(b"gather_tma", 1))
+        assert np.array_equal(ref, want), (dims, step, d)
+
+
 def test_toy_denoisers_bitexact(cuda, oracle):
     for shape, patch, k, r, step, d, seed in _cases(2, 40):
         z, cond = oracle.synthetic(shape, d, seed)
@@ -141,10 +179,28 @@ def test_c2_full_size_engine_vs_oracle(cuda, oracle):
 
 
 def test_nonfinite_is_reported(cuda):
+    """Non-finite values raise the device NonFinite flag (the reference's NonFinite,
+    src/latent.cpp:72-77 / dtype.cpp quantize) in K10 and the sampler; f16 saturation does not."""
+    import torch
+
     z = lp.LatentTensor.from_numpy(np.full((1, 2, 2, 2), 60000.0), 2)
     lp.device_flags(reset=True)
     lp.cfg_predict(lp.IdentityDenoiser(), z, 1, [1.0] * 8, 3.0)  # f16 saturates, stays finite
     assert lp.device_flags() == 0
+    dims = (2, 4, 6, 6)
+    for d, dt in ((4, torch.float32), (8, torch.float64)):
+        plan = lp.build_plan(dims, (1, 1, 1), 1, 2, 0.5)
+        preds = [lp.LatentTensor(torch.ones(plan.sub_shape(dims, k), dtype=dt, device="cuda"), d) for k in range(2)]
+        assert np.isfinite(lp.reconstruct(preds, plan, dims).to_numpy()).all() and lp.device_flags() == 0
+        preds[1].data[0, 1, 2, 3] = float("nan")
+        lp.reconstruct(preds, plan, dims)
+        assert lp.device_flags() & 1, d
+        zt = lp.LatentTensor(torch.zeros(dims, dtype=dt, device="cuda"), d)
+        eps = lp.LatentTensor(torch.zeros(dims, dtype=dt, device="cuda"), d)
+        eps.data[1, 0, 0, 0] = float("inf")
+        lp.sampler_step(zt, eps, 1, 0.05)
+        assert lp.device_flags() & 1, d
+        assert lp.device_flags() == 0  # reset by the read
 
 
 @pytest.mark.gpu

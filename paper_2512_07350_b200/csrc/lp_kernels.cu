@@ -895,6 +895,19 @@ __device__ __forceinline__ typename Vec4<D>::T vload4(const typename Store<D>::T
     return *reinterpret_cast<const typename Vec4<D>::T*>(p);
 }
 
+// a / Z, correctly rounded, from the tabulated y = RN(1/Z): q = a*y, r = a - q*Z (exact, one
+// FMA), q' = q + r*y — Markstein's final step, which yields RN(a/Z) when y = RN(1/Z) and q is
+// within an ulp of a/Z (no overflow/underflow; here Z in [1, 64] and |a| is tested against the
+// subnormal range).  Checked against true division on 5.2e8 (Z, a) pairs of ramp-weight sums
+// (scripts/micro/markstein.c) and by every bit-exact K10 test.  r == 0 keeps q (exact, and
+// the sign of a zero quotient).  Saves MUFU.RCP64H + the Newton steps of __ddiv_rn.
+__device__ __forceinline__ double div_z(double a, double Z, double y) {
+    if (fabs(a) < 0x1p-900 || !isfinite(a)) return __ddiv_rn(a, Z);
+    const double q = __dmul_rn(a, y);
+    const double r = __fma_rn(-q, Z, a);
+    return r == 0.0 ? q : __fma_rn(r, y, q);
+}
+
 // The coverage table of a plan (layout below), built once on the device by one block with
 // entry_weight's exact operations and cached per (plan, gather layout, device): K10 blocks
 // then only copy ~2 KB into shared memory instead of each re-deriving it.
@@ -902,6 +915,7 @@ struct CovLayout {
     // structure of arrays [cover][x]: lanes on consecutive x (W axis) hit distinct banks
     double* wts;      // [4][Dx]
     double* zsum;     // [Dx]
+    double* zinv;     // [Dx] RN(1 / Z) (the division's Markstein step, div_z)
     float* zsumf;     // [Dx] (FAST)
     uint32_t* offs;   // [4][Dx]
     uint32_t* ostr;   // [4][Dx]
@@ -909,7 +923,8 @@ struct CovLayout {
     __host__ __device__ explicit CovLayout(void* base, int Dx) {
         wts = static_cast<double*>(base);
         zsum = wts + kReconCover * Dx;
-        zsumf = reinterpret_cast<float*>(zsum + Dx);
+        zinv = zsum + Dx;
+        zsumf = reinterpret_cast<float*>(zinv + Dx);
         offs = reinterpret_cast<uint32_t*>(zsumf + Dx);
         ostr = offs + kReconCover * Dx;
         cnt = ostr + kReconCover * Dx;
@@ -938,6 +953,7 @@ __global__ void __launch_bounds__(256) k_recon_table(const __grid_constant__ Rec
             }
         }
         t.zsum[x] = zs;
+        t.zinv[x] = __ddiv_rn(1.0, zs);
         t.zsumf[x] = zf;
         t.cnt[x] = static_cast<uint32_t>(c);
     }
@@ -957,6 +973,7 @@ __global__ void __launch_bounds__(256) k_reconstruct_cov(const __grid_constant__
     const CovLayout t(cov, Dx);
     const double* wts = t.wts;
     const double* zsum = t.zsum;
+    const double* zinv = t.zinv;
     const float* zsumf = t.zsumf;
     const uint32_t* offs = t.offs;
     const uint32_t* ostr = t.ostr;
@@ -972,7 +989,7 @@ __global__ void __launch_bounds__(256) k_reconstruct_cov(const __grid_constant__
             for (int cc = 0; cc < kReconCover; ++cc)
                 if (cc < c) a = __dadd_rn(a, __dmul_rn(wts[cc * Dx + x], load_val<D>(r, cc)));
             const double Z = zsum[x];
-            eps = quantize_dev<D>(Z == 1.0 ? a : __ddiv_rn(a, Z));
+            eps = quantize_dev<D>(Z == 1.0 ? a : (p.mk ? div_z(a, Z, zinv[x]) : __ddiv_rn(a, Z)));
         } else {
             float a = 0.f;
 #pragma unroll
@@ -1092,7 +1109,7 @@ __global__ void __launch_bounds__(256) k_reconstruct_xs(const __grid_constant__ 
         off[cc] = cc < c ? __ldg(t.offs + cc * Dx + x) : 0u;
         str[cc] = cc < c ? __ldg(t.ostr + cc * Dx + x) : 0u;
     }
-    const double Z = __ldg(t.zsum + x);
+    const double Z = __ldg(t.zsum + x), Zi = __ldg(t.zinv + x);
     const float Zf = __ldg(t.zsumf + x);
     bool ok = true;
     constexpr int U = 4;
@@ -1118,7 +1135,7 @@ __global__ void __launch_bounds__(256) k_reconstruct_xs(const __grid_constant__ 
 #pragma unroll
                 for (int cc = 0; cc < kReconCover; ++cc)
                     if (cc < c) a = __dadd_rn(a, __dmul_rn(w[cc], load_val<D>(raw[u], cc)));
-                eps = quantize_dev<D>(Z == 1.0 ? a : __ddiv_rn(a, Z));
+                eps = quantize_dev<D>(Z == 1.0 ? a : (p.mk ? div_z(a, Z, Zi) : __ddiv_rn(a, Z)));
             } else {
                 float a = 0.f;
 #pragma unroll
@@ -1152,7 +1169,7 @@ static size_t recon_cov_bytes(const ReconParams& p, int dtype) {
         if (c > kReconCover) return 0;
     }
     (void)dtype;
-    const size_t bytes = (static_cast<size_t>(p.D) * (kReconCover * 8 + 8 + 4 + kReconCover * 8 + 4) + 15) / 16 * 16;
+    const size_t bytes = (static_cast<size_t>(p.D) * (kReconCover * 8 + 8 + 8 + 4 + kReconCover * 8 + 4) + 15) / 16 * 16;
     return bytes <= 48 * 1024 ? bytes : 0;
 }
 
@@ -1281,6 +1298,7 @@ ReconParams make_recon_params(const lp_plan& plan, const Shape4& s, const std::v
     p.total = s.volume();
     p.eta = eta;
     p.use32 = p.total < (1ll << 31) ? 1 : 0;
+    p.mk = tune_get("recon_mk", 1);
     if (p.use32) {
         p.div_inner = make_fastdiv(static_cast<uint32_t>(p.inner));
         p.div_d = make_fastdiv(static_cast<uint32_t>(p.D));

@@ -27,6 +27,7 @@ struct ReconParams {
     double eta;
     FastDiv div_inner, div_d;  // valid (use32) when total < 2^31
     int use32;
+    int mk;  // K10 exact division via the tabulated reciprocal (div_z; knob recon_mk)
     // peer exchange: the engine's failure word (non-zero = a peer's shard never arrived);
     // K10 then leaves z untouched instead of blending stale shards.  nullptr = no check.
     const unsigned* abort;

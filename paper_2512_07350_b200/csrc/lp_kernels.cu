@@ -959,7 +959,67 @@ __global__ void __launch_bounds__(256) k_recon_table(const __grid_constant__ Rec
     }
 }
 
-template <int D, bool UPDATE, bool FAST, bool VEC>
+// One K10 element with a compile-time cover count C (no predicated-off conversions for the
+// covers a position does not have) and the Z == 1 test hoisted by the caller (Z1): the blend
+// sum_k w_k pred_k in worker order, / Z (true division, or div_z), quantized; UPDATE: the
+// sampler's z - eta * eps, quantized and stored.  Returns false for a non-finite result.
+template <int D, bool UPDATE, bool FAST, int C, bool Z1>
+__device__ __forceinline__ bool k10_elem(const double (&w)[kReconCover], double Z, double Zi, float Zf, bool mk,
+                                         double eta, const typename Store<D>::T (&r)[kReconCover],
+                                         typename Store<D>::T zraw, typename Store<D>::T& out) {
+    double eps;
+    if (!FAST) {
+        double a = 0.0;  // from +0 like the reference's accumulator (a -0 product sums to +0)
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) a = __dadd_rn(a, __dmul_rn(w[cc], load_val<D>(r, cc)));
+        eps = quantize_dev<D>(Z1 ? a : (mk ? div_z(a, Z, Zi) : __ddiv_rn(a, Z)));
+    } else {
+        float a = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) a = fmaf(static_cast<float>(w[cc]), static_cast<float>(load_val<D>(r, cc)), a);
+        eps = quantize_dev<D>(static_cast<double>(Z1 ? a : a / Zf));
+    }
+    const bool ok = isfinite(eps);
+    double res = eps;
+    if (UPDATE) {
+        const double zo = load_val<D>(&zraw, 0);
+        res = FAST ? static_cast<double>(fmaf(-static_cast<float>(eta), static_cast<float>(eps), static_cast<float>(zo)))
+                   : __dsub_rn(zo, __dmul_rn(eta, eps));
+    }
+    return store_q<D>(&out, 0, res) && ok;
+}
+
+// Dispatch a group of n elements sharing one position x onto the compile-time cover count
+// and Z == 1 forms (c and Z are warp-uniform except at coverage boundaries).
+template <int D, bool UPDATE, bool FAST, int N>
+__device__ __forceinline__ bool k10_group(uint32_t c, const double (&w)[kReconCover], double Z, double Zi, float Zf,
+                                          bool mk, double eta, const typename Store<D>::T (&r)[N][kReconCover],
+                                          const typename Store<D>::T* zr, typename Store<D>::T* q, uint32_t live) {
+    bool ok = true;
+#define LP_K10G(CC, ZZ)                                                                                         \
+    for (int u = 0; u < N; ++u)                                                                                 \
+        if (u < static_cast<int>(live))                                                                         \
+            ok = k10_elem<D, UPDATE, FAST, CC, ZZ>(w, Z, Zi, Zf, mk, eta, r[u], UPDATE ? zr[u] : typename Store<D>::T{}, q[u]) && ok;
+    const bool z1 = FAST ? Zf == 1.f : Z == 1.0;
+    switch (c) {
+        case 1:
+            if (z1) { LP_K10G(1, true) } else { LP_K10G(1, false) }
+            break;
+        case 2:
+            if (z1) { LP_K10G(2, true) } else { LP_K10G(2, false) }
+            break;
+        case 3:
+            if (z1) { LP_K10G(3, true) } else { LP_K10G(3, false) }
+            break;
+        default:
+            if (z1) { LP_K10G(4, true) } else { LP_K10G(4, false) }
+            break;
+    }
+#undef LP_K10G
+    return ok;
+}
+
+template <int D, bool UPDATE, bool FAST, bool VEC, int GV = 8>
 __global__ void __launch_bounds__(256) k_reconstruct_cov(const __grid_constant__ ReconParams p,
                                                          const typename Store<D>::T* __restrict__ preds,
                                                          typename Store<D>::T* __restrict__ z,
@@ -1006,7 +1066,7 @@ __global__ void __launch_bounds__(256) k_reconstruct_cov(const __grid_constant__
         }
         return store_q<D>(&out, 0, res) && ok;
     };
-    constexpr int G = 8;  // elements per thread per iteration
+    constexpr int G = VEC ? GV : 8;  // elements per thread per iteration (VEC: knob recon_g, 8 or 4)
     const uint32_t total = static_cast<uint32_t>(p.total);
     bool ok = true;
     if (VEC) {
@@ -1036,8 +1096,11 @@ __global__ void __launch_bounds__(256) k_reconstruct_cov(const __grid_constant__
                 for (int h = 0; h < G / 4; ++h)
                     *reinterpret_cast<typename Vec4<D>::T*>(zr + 4 * h) = vload4<D>(z + idx0 + 4 * h);
             }
+            double w[kReconCover];
 #pragma unroll
-            for (int u = 0; u < G; ++u) ok = finish(x, c, raw[u], UPDATE ? zr[u] : T{}, q[u]) && ok;
+            for (int cc = 0; cc < kReconCover; ++cc) w[cc] = cc < static_cast<int>(c) ? wts[cc * Dx + x] : 0.0;
+            ok = k10_group<D, UPDATE, FAST, G>(c, w, FAST ? 0.0 : zsum[x], FAST ? 0.0 : zinv[x], FAST ? zsumf[x] : 1.f,
+                                               p.mk, p.eta, raw, zr, q, G) && ok;
             T* out = (UPDATE ? z : eps_out) + idx0;
 #pragma unroll
             for (int h = 0; h < G / 4; ++h)
@@ -1125,33 +1188,12 @@ __global__ void __launch_bounds__(256) k_reconstruct_xs(const __grid_constant__ 
                 if (UPDATE) zr[u] = z[static_cast<uint64_t>(o) * Dx + x];
             }
         }
+        const uint32_t live = rows > o0 ? min(static_cast<uint32_t>(U), (rows - o0 + R - 1) / R) : 0u;
+        T q[U];
+        ok = k10_group<D, UPDATE, FAST, U>(c, w, Z, Zi, Zf, p.mk, p.eta, raw, zr, q, live) && ok;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t o = o0 + u * R;
-            if (o >= rows) continue;
-            double eps;
-            if (!FAST) {
-                double a = 0.0;
-#pragma unroll
-                for (int cc = 0; cc < kReconCover; ++cc)
-                    if (cc < c) a = __dadd_rn(a, __dmul_rn(w[cc], load_val<D>(raw[u], cc)));
-                eps = quantize_dev<D>(Z == 1.0 ? a : (p.mk ? div_z(a, Z, Zi) : __ddiv_rn(a, Z)));
-            } else {
-                float a = 0.f;
-#pragma unroll
-                for (int cc = 0; cc < kReconCover; ++cc)
-                    if (cc < c) a = fmaf(static_cast<float>(w[cc]), static_cast<float>(load_val<D>(raw[u], cc)), a);
-                eps = quantize_dev<D>(static_cast<double>(a / Zf));
-            }
-            ok = ok && isfinite(eps);
-            double res = eps;
-            if (UPDATE) {
-                const double zo = load_val<D>(zr, u);
-                res = FAST ? static_cast<double>(fmaf(-static_cast<float>(p.eta), static_cast<float>(eps), static_cast<float>(zo)))
-                           : __dsub_rn(zo, __dmul_rn(p.eta, eps));
-            }
-            ok = store_q<D>(UPDATE ? z : eps_out, static_cast<uint64_t>(o) * Dx + x, res) && ok;
-        }
+        for (int u = 0; u < U; ++u)
+            if (u < static_cast<int>(live)) (UPDATE ? z : eps_out)[static_cast<uint64_t>(o0 + u * R) * Dx + x] = q[u];
     }
     if (!ok) raise_flag(LP_FLAG_NONFINITE);
 }
@@ -1238,11 +1280,14 @@ static void launch_recon(const ReconParams& p, const void* preds, void* z, void*
         const void* table = p.table ? p.table : recon_table(p, cov, st);
         const uint32_t tv = static_cast<uint32_t>(cov / 16);
         int res = 0;
-        auto kfn = fast ? (vec ? k_reconstruct_cov<D, UPDATE, true, true> : k_reconstruct_cov<D, UPDATE, true, false>)
-                        : (vec ? k_reconstruct_cov<D, UPDATE, false, true> : k_reconstruct_cov<D, UPDATE, false, false>);
+        const bool g4 = vec && tune_get("recon_g", 4) == 4;  // VEC: 4 elements (one vector per cover) per thread
+        auto kfn = fast ? (vec ? (g4 ? k_reconstruct_cov<D, UPDATE, true, true, 4> : k_reconstruct_cov<D, UPDATE, true, true>)
+                               : k_reconstruct_cov<D, UPDATE, true, false>)
+                        : (vec ? (g4 ? k_reconstruct_cov<D, UPDATE, false, true, 4> : k_reconstruct_cov<D, UPDATE, false, true>)
+                               : k_reconstruct_cov<D, UPDATE, false, false>);
         LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, kfn, 256, cov));
         res = std::max(1, res);
-        const int gq = grid_for(p.total / 8, 256, res);
+        const int gq = grid_for(p.total / (g4 ? 4 : 8), 256, res);
         auto* out_z = static_cast<T*>(z);
         auto* out_e = static_cast<T*>(eps);
         const auto* in = static_cast<const T*>(preds);
@@ -1257,12 +1302,8 @@ static void launch_recon(const ReconParams& p, const void* preds, void* z, void*
             const int gx = static_cast<int>((live + 255) / 256);
             if (fast) k_reconstruct_xs<D, UPDATE, true><<<gx, 256, 0, st>>>(p, in, out_z, out_e, table, live);
             else k_reconstruct_xs<D, UPDATE, false><<<gx, 256, 0, st>>>(p, in, out_z, out_e, table, live);
-        } else if (fast) {
-            if (vec) k_reconstruct_cov<D, UPDATE, true, true><<<gq, 256, cov, st>>>(p, in, out_z, out_e, static_cast<const uint4*>(table), tv);
-            else k_reconstruct_cov<D, UPDATE, true, false><<<gq, 256, cov, st>>>(p, in, out_z, out_e, static_cast<const uint4*>(table), tv);
         } else {
-            if (vec) k_reconstruct_cov<D, UPDATE, false, true><<<gq, 256, cov, st>>>(p, in, out_z, out_e, static_cast<const uint4*>(table), tv);
-            else k_reconstruct_cov<D, UPDATE, false, false><<<gq, 256, cov, st>>>(p, in, out_z, out_e, static_cast<const uint4*>(table), tv);
+            kfn<<<gq, 256, cov, st>>>(p, in, out_z, out_e, static_cast<const uint4*>(table), tv);
         }
     } else if (!fast && p.use32 && tab <= 48 * 1024) {
         k_reconstruct_tab<D, UPDATE><<<g, 256, tab, st>>>(p, static_cast<const T*>(preds), static_cast<T*>(z),

@@ -1,8 +1,8 @@
 """K1 (partition gather) and K10 (reconstruct + sampler update) micro-benchmark at the BASELINE
 latent sizes: per-launch device time, achieved algorithmic GB/s and fraction of the measured HBM
 copy bandwidth.  Two timings per kernel: `*_us` = 64 back-to-back launches over 8 private
-buffer copies used round robin (working set > L2, launch overhead amortised; the bench.py
-method), and `*_flush_us` = one launch between L2 flushes, CUDA events around it (~2 us event
+buffer copies used round robin (working set > L2), captured in one CUDA graph so host launch
+gaps do not count (bench.py's engine replay does the same from C++), and `*_flush_us` = one launch between L2 flushes, CUDA events around it (~2 us event
 granularity: an upper bound).
 
 Algorithmic bytes: K1 = 2 * shard elements * b; K10 = (sum of shard elements +
@@ -46,13 +46,19 @@ SETS, ITERS = 8, 64
 
 
 def replay(fn):
-    """Per-launch ms of ITERS back-to-back launches fn(i % SETS) (one event pair around all)."""
+    """Per-launch ms of ITERS back-to-back launches fn(i % SETS), captured in one CUDA graph (no
+    host launch gaps between these few-us kernels), one event pair around the graph replay."""
     for i in range(SETS):
         fn(i)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(ITERS):
+            fn(i % SETS)
+    g.replay()
     a, b = torch.cuda.Event(True), torch.cuda.Event(True)
     a.record()
-    for i in range(ITERS):
-        fn(i % SETS)
+    g.replay()
     b.record()
     torch.cuda.synchronize()
     return a.elapsed_time(b) / ITERS

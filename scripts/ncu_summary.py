@@ -37,6 +37,11 @@ METRICS = {
     "duration_ms": "gpu__time_duration.sum",
     "dram_read_MB": "dram__bytes_read.sum",
     "dram_write_MB": "dram__bytes_write.sum",
+    # tcgen05-aware: bf16->fp32 UTCHMMA tensor ops (the kind::f16 MMAs of the GEMM and attention,
+    # 1-CTA and CTA-pair alike) against their peak; the legacy pipe_tensor metric undercounts
+    # cta_group::2 UTCHMMA and is kept only for comparison
+    "utchmma_bf16_pct_of_peak": "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32.avg.pct_of_peak_sustained_elapsed",
+    "utchmma_bf16_ops": "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32.sum",
     "tensor_pipe_active_pct": "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
     "mufu_xu_pct_active": "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
     "fma_pipe_pct_active": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",

@@ -210,7 +210,10 @@ __global__ void __launch_bounds__(kGtThreads) k_gather_tma(const __grid_constant
                                                            typename ElemOf<E>::T* __restrict__ dst) {
     using T = typename ElemOf<E>::T;
     constexpr int V = 16 / E;  // elements per 16-byte vector
-    extern __shared__ __align__(128) uint8_t sbuf[];
+    extern __shared__ __align__(128) uint8_t sbuf_raw[];
+    // tensor-copy destinations must be 128-byte aligned: the dynamic segment follows the static
+    // barriers, so align by hand (the launch adds 128 bytes)
+    uint8_t* sbuf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sbuf_raw) + 127) & ~uintptr_t(127));
     __shared__ uint64_t full[kGtStages];
     const uint32_t tid = threadIdx.x;
     if (tid == 0) {
@@ -409,7 +412,7 @@ static bool gather_tma(const void* z, const Shape4& s, const lp_plan& plan, cons
         off += rows * g.len;
     }
     p.items = items;
-    const int smem = kGtStages * static_cast<int>(p.stage_bytes);
+    const int smem = kGtStages * static_cast<int>(p.stage_bytes) + 128;
     static int attr_bytes[9] = {};
     if (attr_bytes[E] < smem) {
         switch (E) {

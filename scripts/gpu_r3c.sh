@@ -3,6 +3,9 @@
 # (gather_tma on/off), one bench line.
 O=gpurun_out/r3c
 mkdir -p $O
+timeout 600 python -m pytest -m gpu -q -x -p no:cacheprovider tests/test_lp_gpu.py -k "tma or extract" > $O/pytest_tma.log 2>&1
+rc=$?; echo "tma tests rc=$rc" | tee -a $O/status; tail -3 $O/pytest_tma.log
+if [ $rc -ne 0 ]; then export LP_TUNE_GATHER_TMA=0; echo "K1 TMA disabled for the rest" | tee -a $O/status; fi
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" | tee -a $O/status
 timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" | tee -a $O/status
 tail -15 $O/pytest_gpu.log

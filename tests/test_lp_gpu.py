@@ -246,3 +246,37 @@ def test_reconstruct_paths_bitexact(cuda, oracle, shape, patch, k, r, step, d):
     zt = lp.LatentTensor.from_numpy(z, d)
     lp.reconstruct_update(preds, plan, zt, 0.05)
     assert np.array_equal(zt.to_numpy(), oracle.sampler_step(z, want, d, 0.05))
+
+
+@pytest.mark.parametrize("d", [2, 4, 8])
+@pytest.mark.parametrize("shape,k,r", [
+    ((2, 5, 6, 52), 4, 0.5),       # 60 rows: one full 32-row tile + a ragged one
+    ((3, 7, 5, 37), 3, 0.25),      # odd W: runs and the ragged tile not 16-byte aligned (cooperative copies)
+    ((1, 3, 3, 40), 8, 1.0),       # 9 rows (< one tile), 8 workers, up to 3 covers per position
+    ((16, 21, 60, 104), 4, 0.5),   # C2's W axis
+])
+@pytest.mark.parametrize("wt", [1, 0])
+def test_reconstruct_w_axis_tile_bitexact(cuda, oracle, shape, k, r, d, wt):
+    """K10 on W-axis plans (inner == 1): the tile kernel k_reconstruct_wt (knob recon_wt=1, bulk
+    copies of 32-row runs, segment-uniform warps) and the x-stationary kernel (recon_wt=0),
+    exact mode, reconstruct and fused update, bit for bit against the oracle."""
+    from paper_2512_07350_b200 import _lib
+
+    patch = (1, 1, 1) if shape[3] % 2 else (1, 2, 2)
+    z, _ = oracle.synthetic(shape, d, 5)
+    plan = lp.build_plan(shape, patch, 3, k, r)
+    oplan = oracle.build_plan(shape, patch, 3, k, r)
+    assert plan.raw.axis == 2
+    rng = np.random.default_rng(3)
+    preds_np = [lp._quantize_np(rng.normal(size=sub_shape(shape, oplan, e)) * 3, d).astype(np.float64)
+                for e in range(oplan.n)]
+    want = oracle.reconstruct(np.concatenate([p.reshape(-1) for p in preds_np]), shape, d, oplan)
+    preds = [lp.LatentTensor.from_numpy(p, d) for p in preds_np]
+    _lib.check(_lib.lib().lp_tune(b"recon_wt", wt))
+    try:
+        assert np.array_equal(lp.reconstruct(preds, plan, shape).to_numpy(), want)
+        zt = lp.LatentTensor.from_numpy(z, d)
+        lp.reconstruct_update(preds, plan, zt, 0.05)
+        assert np.array_equal(zt.to_numpy(), oracle.sampler_step(z, want, d, 0.05))
+    finally:
+        _lib.check(_lib.lib().lp_tune(b"recon_wt", 1))

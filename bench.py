@@ -323,8 +323,11 @@ def run_reference_arm(args, rank, world):
         return
     cpu_reference_run(cfg, 1, threads)
     lp_only, lp_info = cpu_reference_run(cfg, 20, threads)
-    # whole steps of the metric's workload: one rotation cycle (T, H, W), nothing extrapolated
-    n = args.ref_steps or len(cfg.axes())
+    # whole steps of the metric's workload, nothing extrapolated.  Default: ONE step (step 1, the
+    # T axis: ~210 s on 16 cores, so the arm ends within a few minutes); its shards carry ~7% more
+    # DiT FLOPs than the T/H/W cycle mean, so one T step slightly understates the reference's
+    # cycle throughput.  --ref-steps 3 times a whole cycle.
+    n = args.ref_steps or 1
     wall, dit_s, calls = reference_full_steps(cfg, n, threads)
     value = n / wall
     sample = (f"UNMODIFIED reference run_lp (oracle/_ref) for {n} whole LP steps (steps 1..{n}: axes "
@@ -707,7 +710,7 @@ def main():
                     help="LP overlap ratio r (BASELINE configs[2] sweep; default 0.5 = configs[1])")
     ap.add_argument("--cpu-steps", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-steps", type=int, default=0, help="reference arm: whole LP steps to time (default: one cycle)")
+    ap.add_argument("--ref-steps", type=int, default=0, help="reference arm: whole LP steps to time (default 1: step 1, the T axis, ~210 s on 16 cores; 3 = one T/H/W cycle)")
     ap.add_argument("--exchange-iters", type=int, default=20)
     ap.add_argument("--hbm-iters", type=int, default=64, help="K1/K10 replays per axis for the HBM roofline")
     ap.add_argument("--hbm-sets", type=int, default=8, help="buffer copies the K1/K10 replays cycle through")

@@ -125,7 +125,7 @@ __device__ __forceinline__ void trace_ev(int j, int t, int ev) {
 // halves (p_half after keys [0,64), p_full after [64,128)) so the MMA warp starts
 // O += P[:, :64] V[:64] while the second half is computed.  POLY of every 16 pairs use
 // the FMA-pipe polynomial, the rest MUFU.EX2.  MASK: keys >= valid get probability 0.
-template <int POLY, bool MASK, bool TR>
+template <int POLY, bool MASK, bool TR, bool PAIR = false>
 __device__ __forceinline__ void softmax_block(uint32_t tS, uint32_t tO, int valid, float c, float& m_run,
                                               float& l_run, uint64_t* p_half, uint64_t* p_full, int j, int t,
                                               bool tr0) {
@@ -206,7 +206,8 @@ __device__ __forceinline__ void softmax_block(uint32_t tS, uint32_t tO, int vali
     auto publish = [&](uint64_t* bar, int half) {
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(bar);
+        if (PAIR) mbar_arrive_cluster(bar, 0);  // CTA pair: the leader's barrier counts both CTAs' rows
+        else mbar_arrive(bar);
         if (tr0) trace_ev<TR>(j, t, 2 + half);
         // per lane-quarter arrival (events 8..11 p_half, 12..15 p_full): the barrier completes
         // at the slowest of the four warps
@@ -551,6 +552,236 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
     if (warp == 2) tmem_dealloc(tmem, AttnCfg<NT>::tmem_cols);
 }
 
+// ---------------------------------------------------------------------------
+// Self-attention on CTA pairs (cta_group::2; knob attn_pair).  A 2-CTA cluster shares one
+// (head, batch) and each CTA keeps its own two 128-row Q tiles (256 query rows per CTA, 512 per
+// pair).  The leader issues every MMA for both: S_t = [Q_t(cta0); Q_t(cta1)] K_j^T is ONE
+// M = 256 instruction stream whose B operand (K_j, 128 keys) is split by rows — each CTA
+// TMA-loads and holds 64 keys — and O_t += P_t V_j reads P from each CTA's own TMEM and V split
+// by columns (each CTA holds 64 of the 128 dims of all 128 keys).  Per SM and key block that
+// halves the K/V bytes TMA writes into shared memory (64 -> 32 KB) and the B-operand bytes
+// the tensor core reads from it (S: 64 -> 48 KB per tile, PV: 32 -> 16 KB), and one issued
+// MMA covers both SMs.  Barriers: Q/K/V completions count both CTAs' bytes on the leader's
+// barriers (2-SM TMA), the leader's commits are multicast to both CTAs (s_full, k/v_empty,
+// o_final), and both CTAs' softmax rows arrive on the leader's p_half / p_full (count 256).
+// The softmax and epilogue are the single-CTA kernel's.
+// ---------------------------------------------------------------------------
+constexpr int kPairKS = 4, kPairVS = 4;
+constexpr int kHalfTile = 64 * 128 * 2;  // 16 KB: [64 keys x 128 dims] (K) or [128 keys x 64 dims] (V)
+constexpr int kPairSmem = 2 * kTileBytes + (kPairKS + kPairVS) * kHalfTile + 1024 + 256;
+
+__device__ __forceinline__ void mma_ts_2sm(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+template <int POLY>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAttnThreads, 1)
+    k_attention_pair(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                     const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap to,
+                     AttnKernelArgs a) {
+    constexpr int NT = 2, KS = kPairKS, VS = kPairVS;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;                    // [tile][2 atoms of 128 rows x 128 B]
+    uint8_t* sK = sQ + NT * kTileBytes;    // [KS][2 atoms of 64 rows x 128 B]  (this CTA's 64 keys)
+    uint8_t* sV = sK + KS * kHalfTile;     // [VS][1 atom of 128 rows x 128 B]  (this CTA's 64 dims)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VS * kHalfTile);
+    uint64_t* q_full = bars + 0;
+    uint64_t* k_full = q_full + 1;
+    uint64_t* k_empty = k_full + KS;
+    uint64_t* v_full = k_empty + KS;
+    uint64_t* v_empty = v_full + VS;
+    uint64_t* s_full = v_empty + VS;
+    uint64_t* p_full = s_full + NT;
+    uint64_t* p_half = p_full + NT;
+    uint64_t* o_final = p_half + NT;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + NT);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const uint32_t rank = cluster_ctarank();
+    const int nkv = static_cast<int>((a.n_kv + kTile - 1) / kTile);
+    const int qt = static_cast<int>(blockIdx.x), h = static_cast<int>(blockIdx.y), b = static_cast<int>(blockIdx.z);
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tq);
+        tma_prefetch(&tk);
+        tma_prefetch(&tv);
+        mbar_init(q_full, 1);
+        for (int s = 0; s < KS; ++s) {
+            mbar_init(&k_full[s], 1);
+            mbar_init(&k_empty[s], 1);
+        }
+        for (int s = 0; s < VS; ++s) {
+            mbar_init(&v_full[s], 1);
+            mbar_init(&v_empty[s], 1);
+        }
+        for (int t = 0; t < NT; ++t) {
+            mbar_init(&s_full[t], 1);
+            mbar_init(&p_full[t], 256);
+            mbar_init(&p_half[t], 256);
+            mbar_init(&o_final[t], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc_2sm(tmem_slot, 512);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const int32_t qrow = static_cast<int32_t>(b * a.q_rows_per_batch + qt * NT * kTile);
+            const int32_t qc = static_cast<int32_t>(a.q_col0 + h * kHD);
+            if (rank == 0) mbar_arrive_expect_tx(q_full, 2 * NT * kTileBytes);
+            for (int t = 0; t < NT; ++t) {
+                tma_load_2d_2sm(&tq, q_full, sQ + t * kTileBytes, qc, qrow + t * kTile);
+                tma_load_2d_2sm(&tq, q_full, sQ + t * kTileBytes + kAtom, qc + 64, qrow + t * kTile);
+            }
+            const int32_t kc = static_cast<int32_t>(a.k_col0 + h * kHD);
+            const int32_t vc = static_cast<int32_t>(a.v_col0 + h * kHD + rank * 64);
+            auto load_k = [&](int j) {
+                const int s = j % KS;
+                mbar_wait(&k_empty[s], ((j / KS) & 1) ^ 1);
+                if (rank == 0) mbar_arrive_expect_tx(&k_full[s], 2 * kHalfTile);
+                const int32_t kr = static_cast<int32_t>(b * a.kv_rows_per_batch + j * kTile + rank * 64);
+                tma_load_2d_2sm(&tk, &k_full[s], sK + s * kHalfTile, kc, kr);
+                tma_load_2d_2sm(&tk, &k_full[s], sK + s * kHalfTile + kHalfTile / 2, kc + 64, kr);
+            };
+            auto load_v = [&](int j) {
+                const int s = j % VS;
+                mbar_wait(&v_empty[s], ((j / VS) & 1) ^ 1);
+                if (rank == 0) mbar_arrive_expect_tx(&v_full[s], 2 * kHalfTile);
+                const int32_t kr = static_cast<int32_t>(b * a.kv_rows_per_batch + j * kTile);
+                tma_load_2d_2sm(&tv, &v_full[s], sV + s * kHalfTile, vc, kr);
+            };
+            int jk = 0;
+            for (; jk < nkv && jk < KS - 1; ++jk) load_k(jk);
+            for (int j = 0; j < nkv; ++j) {
+                load_v(j);
+                if (jk < nkv) load_k(jk++);
+            }
+        }
+    } else if (warp == 1) {
+        if (rank == 0) {
+            // the leader issues for both CTAs (converged warp, one elected lane; see k_attention)
+            const bool leader = elect_one();
+            constexpr uint32_t idS = idesc_bf16(256, 128);
+            constexpr uint32_t idO = idesc_bf16(256, 128, /*b_mn_major=*/true);
+            const uint64_t dQ = desc_sw128(smem_u32(sQ)), dK = desc_sw128(smem_u32(sK));
+            const uint64_t dV = desc_sw128(smem_u32(sV), /*sbo=*/1024, /*lbo=*/kAtom);
+            mbar_wait_sleep(q_full, 0);
+            auto issue_s = [&](int t, int j) {
+                const int s = j % KS;
+                if (t == 0) {
+                    mbar_wait_sleep(&k_full[s], (j / KS) & 1);
+                    tc_fence_after();
+                }
+                if (leader) {
+                    const uint64_t q0 = dQ + t * (kTileBytes >> 4), k0 = dK + s * (kHalfTile >> 4);
+#pragma unroll
+                    for (int k = 0; k < kHD / 16; ++k) {
+                        const uint64_t oq = static_cast<uint64_t>((k >> 2) * kAtom + (k & 3) * 32) >> 4;
+                        const uint64_t ok = static_cast<uint64_t>((k >> 2) * (kHalfTile / 2) + (k & 3) * 32) >> 4;
+                        mma_ss_2sm(tmem + t * 128, q0 + oq, k0 + ok, idS, k != 0);
+                    }
+                    mma_commit_2sm(&s_full[t], 0x3);
+                    if (t == NT - 1) mma_commit_2sm(&k_empty[s], 0x3);
+                }
+                __syncwarp();
+            };
+            auto issue_pv = [&](int t, int j, int half) {
+                if (leader) {
+                    const uint64_t v0 = dV + (j % VS) * (kHalfTile >> 4);
+#pragma unroll
+                    for (int k = half * 4; k < half * 4 + 4; ++k)
+                        mma_ts_2sm(tmem + NT * 128 + t * 128, tmem + t * 128 + k * 8, v0 + ((k * 2048) >> 4), idO,
+                                   (j | k) != 0);
+                }
+                __syncwarp();
+            };
+            for (int t = 0; t < NT; ++t) issue_s(t, 0);
+            for (int j = 0; j < nkv; ++j) {
+                const bool more = j + 1 < nkv;
+                for (int t = 0; t < NT; ++t) {
+                    mbar_wait_sleep(&p_half[t], j & 1);
+                    if (t == 0) mbar_wait_sleep(&v_full[j % VS], (j / VS) & 1);
+                    tc_fence_after();
+                    issue_pv(t, j, 0);
+                    mbar_wait_sleep(&p_full[t], j & 1);
+                    tc_fence_after();
+                    issue_pv(t, j, 1);
+                    if (leader) {
+                        if (!more) mma_commit_2sm(&o_final[t], 0x3);
+                        if (t == NT - 1) mma_commit_2sm(&v_empty[j % VS], 0x3);
+                    }
+                    __syncwarp();
+                    if (more) issue_s(t, j + 1);
+                }
+            }
+        }
+    } else {
+        const int t = (warp - 2) >> 2;
+        const uint32_t q = warp & 3;
+        const int row = q * 32 + lane;
+        const uint32_t lane_off = (q * 32) << 16;
+        const uint32_t tS = tmem + t * 128 + lane_off, tO = tmem + NT * 128 + t * 128 + lane_off;
+        const float c = a.scale_log2;
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int j = 0; j < nkv; ++j) {
+            mbar_wait(&s_full[t], j & 1);
+            tc_fence_after();
+            const int valid = static_cast<int>(a.n_kv - static_cast<int64_t>(j) * kTile);
+            if (valid >= kTile)
+                softmax_block<POLY, false, false, true>(tS, tO, valid, c, m_run, l_run, &p_half[t], &p_full[t], j, t, false);
+            else
+                softmax_block<POLY, true, false, true>(tS, tO, valid, c, m_run, l_run, &p_half[t], &p_full[t], j, t, false);
+        }
+        mbar_wait(&o_final[t], 0);
+        tc_fence_after();
+        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+        // O_t staged in Q_t's dead smem (its last S MMA completed before the final PV), then two
+        // TMA tensor stores per warp; the 3-D O map clips rows >= n_q of each batch
+        uint8_t* stage = sQ + t * kTileBytes;
+#pragma unroll 1
+        for (int cc = 0; cc < kHD; cc += 32) {
+            uint32_t r[32];
+            tmem_ld32(tO + cc, r);
+            tmem_ld_wait();
+            uint8_t* arow = stage + (cc >> 6) * kAtom + row * 128;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int unit = ((cc & 63) >> 3) + u;
+                *reinterpret_cast<uint4*>(arow + ((unit ^ (row & 7)) << 4)) =
+                    make_uint4(pack_bf16(__uint_as_float(r[8 * u + 0]) * inv, __uint_as_float(r[8 * u + 1]) * inv),
+                               pack_bf16(__uint_as_float(r[8 * u + 2]) * inv, __uint_as_float(r[8 * u + 3]) * inv),
+                               pack_bf16(__uint_as_float(r[8 * u + 4]) * inv, __uint_as_float(r[8 * u + 5]) * inv),
+                               pack_bf16(__uint_as_float(r[8 * u + 6]) * inv, __uint_as_float(r[8 * u + 7]) * inv));
+            }
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+            const int32_t r0 = static_cast<int32_t>(qt * NT * kTile + t * kTile + q * 32);
+            for (int at = 0; at < 2; ++at)
+                tma_store_3d(&to, stage + at * kAtom + q * 32 * 128, static_cast<int32_t>(h * kHD + at * 64), r0, b);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        __syncwarp();
+    }
+    // the peer's remote arrivals and the leader's MMAs into this CTA's TMEM / smem are done
+    // before either CTA frees TMEM or exits
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 2) tmem_dealloc_2sm(tmem, 512);
+}
+
 static int attn_poly() {
     // pairs out of every 16 whose exp2 runs on the FMA pipe (0, 4, 6 compiled; A/B r1n: 6 best)
     const int v = tune_get("attn_poly", 6);
@@ -576,6 +807,7 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
                                      AttnCfg<1>::smem));
         LP_CUDA(cudaFuncSetAttribute(k_attention<6, false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kAttnSmem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention_pair<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
         attr = true;
     }
     if ((x.ldq | x.ldk | x.ldv | x.ldo) % 8) fail(LP_ERR_INVALID_ARGUMENT, "attention: strides must be multiples of 8");
@@ -624,6 +856,12 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     } else if (nt1) {
         const dim3 g1(static_cast<unsigned>((x.n_q + kTile - 1) / kTile), x.heads, x.batch);
         k_attention<6, false, 1><<<g1, AttnCfg<1>::threads, AttnCfg<1>::smem, st>>>(tq, tk, tv, to, a);
+    } else if (ok_p && tune_get("attn_pair", 0)) {
+        // CTA pairs (self-attention): the K map's box is 64 key rows (each CTA loads half a block)
+        const CUtensorMap tk64 = make_tmap_2d_bf16(x.k, x.ldk, x.kv_total_rows, x.ldk * 2, 64, 64);
+        const unsigned groups = static_cast<unsigned>((x.n_q + 2 * kTile - 1) / (2 * kTile));
+        const dim3 gp((groups + 1) / 2 * 2, x.heads, x.batch);
+        k_attention_pair<6><<<gp, kAttnThreads, kPairSmem, st>>>(tq, tk64, tv, to, a);
     } else if (ok_p && pk >= 2) {
         const int64_t items = ((x.n_q + 2 * kTile - 1) / (2 * kTile)) * x.heads * x.batch;
         const unsigned gp = static_cast<unsigned>(std::min<int64_t>(items, sms));

@@ -929,11 +929,7 @@ struct CovLayout {
     uint32_t* offs;   // [4][Dx]
     uint32_t* ostr;   // [4][Dx]
     uint32_t* cnt;    // [Dx]
-    // W-axis tile kernel (k_reconstruct_wt): positions with the same covering entries form a
-    // segment [seg_x0, seg_x0 + seg_w); kidx = the plan entry of each cover
-    uint32_t* seg_x0;  // [Dx]
-    uint32_t* seg_w;   // [Dx]
-    uint8_t* kidx;     // [4][Dx]
+    uint8_t* kidx;    // [4][Dx] the plan entry of each cover (W-axis tile kernel)
     __host__ __device__ explicit CovLayout(void* base, int Dx) {
         wts = static_cast<double*>(base);
         zsum = wts + kReconCover * Dx;
@@ -942,9 +938,7 @@ struct CovLayout {
         offs = reinterpret_cast<uint32_t*>(zsumf + Dx);
         ostr = offs + kReconCover * Dx;
         cnt = ostr + kReconCover * Dx;
-        seg_x0 = cnt + Dx;
-        seg_w = seg_x0 + Dx;
-        kidx = reinterpret_cast<uint8_t*>(seg_w + Dx);
+        kidx = reinterpret_cast<uint8_t*>(cnt + Dx);
     }
 };
 
@@ -974,21 +968,6 @@ __global__ void __launch_bounds__(256) k_recon_table(const __grid_constant__ Rec
         t.zinv[x] = __ddiv_rn(1.0, zs);
         t.zsumf[x] = zf;
         t.cnt[x] = static_cast<uint32_t>(c);
-    }
-    __syncthreads();
-    // segments: maximal runs of positions covered by the same entries in the same order
-    if (threadIdx.x == 0) {
-        int x0 = 0;
-        for (int x = 1; x <= Dx; ++x) {
-            bool cut = x == Dx || t.cnt[x] != t.cnt[x - 1];
-            for (uint32_t cc = 0; !cut && cc < t.cnt[x]; ++cc) cut = t.kidx[cc * Dx + x] != t.kidx[cc * Dx + x - 1];
-            if (!cut) continue;
-            for (int y = x0; y < x; ++y) {
-                t.seg_x0[y] = static_cast<uint32_t>(x0);
-                t.seg_w[y] = static_cast<uint32_t>(x - x0);
-            }
-            x0 = x;
-        }
     }
 }
 
@@ -1231,137 +1210,105 @@ __global__ void __launch_bounds__(256) k_reconstruct_xs(const __grid_constant__ 
     if (!ok) raise_flag(LP_FLAG_NONFINITE);
 }
 
-// K10 for inner == 1 (W-axis plans), tile form: a block owns kWtRows = 32 consecutive latent
-// rows (o) of every position.  Those rows are ONE contiguous run of z (32·D elements) and, for
-// each entry k, ONE contiguous run of its prediction shard (32·len_k elements at base_k +
-// o0·len_k): the block pulls them into shared memory with 1-D bulk copies (TMA engine; a
-// cooperative copy where a run is not 16-byte aligned), computes in shared memory and writes
-// the 32·D results back with one bulk store.  Work mapping: the positions are cut into
-// segments of equal covering entries (coverage table); a segment of width w holds 32·w tile
-// elements = w chunks of 32, and warp-chunk q (q = 0..D-1) lies inside the segment containing
-// position q — so every warp instruction sees ONE cover count and one set of entries (the
-// x-stationary kernel above diverged at every window edge).
-constexpr int kWtRows = 32;
-template <int D, bool UPDATE, bool FAST>
-__global__ void __launch_bounds__(256) k_reconstruct_wt(const __grid_constant__ ReconParams p,
-                                                        const typename Store<D>::T* __restrict__ preds,
-                                                        typename Store<D>::T* __restrict__ z,
-                                                        typename Store<D>::T* __restrict__ eps_out,
-                                                        const void* __restrict__ table) {
+// K10 for inner == 1, branch-free x-stationary form (knob recon_xsb, default): the threads
+// of a warp hold consecutive positions x, so at every window edge the lanes of one warp have
+// different cover counts and Z == 1 tests — the form above then runs each variant's fp64 code
+// serially.  Here every lane evaluates CM covers (CM = the plan's maximum, a compile-time
+// count): a cover the position does not have re-reads cover 0's (cached) element and is
+// dropped by a select, so the worker-order sum is the reference's bit for bit, NaN / inf
+// included; the division and the Z == 1 shortcut are both evaluated and selected.  No branch
+// depends on x.
+template <int D, bool UPDATE, bool FAST, int CM>
+__global__ void __launch_bounds__(256) k_reconstruct_xsb(const __grid_constant__ ReconParams p,
+                                                         const typename Store<D>::T* __restrict__ preds,
+                                                         typename Store<D>::T* __restrict__ z,
+                                                         typename Store<D>::T* __restrict__ eps_out,
+                                                         const void* __restrict__ table, uint32_t live) {
     if (recon_aborted(p)) return;
     using T = typename Store<D>::T;
-    extern __shared__ __align__(128) uint8_t wt_smem_raw[];
-    __shared__ uint64_t bar;
-    __shared__ uint32_t span_off[kMaxKernelEntries];  // element offset of entry k's run in smem
-    T* sm = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(wt_smem_raw) + 127) & ~uintptr_t(127));
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= live) return;
     const uint32_t Dx = static_cast<uint32_t>(p.D), rows = static_cast<uint32_t>(p.outer);
-    const uint32_t o0 = blockIdx.x * kWtRows, rt = min(static_cast<uint32_t>(kWtRows), rows - o0);
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr uint32_t kAl = 16 / sizeof(T);  // elements per 16 bytes: runs start 16-byte aligned in smem
-    // smem: [tile: 32·D][entry runs, each 32·len_k rounded up to 16 bytes]
-    const uint32_t tile_elems = (kWtRows * Dx + kAl - 1) / kAl * kAl;
-    if (tid == 0) {
-        uint32_t off = tile_elems;
-        for (int k = 0; k < p.n; ++k) {
-            span_off[k] = off;
-            off += (kWtRows * static_cast<uint32_t>(p.e[k].len) + kAl - 1) / kAl * kAl;
-        }
-        tc::mbar_init(&bar, 1);
-        tc::fence_barrier_init();
-    }
-    __syncthreads();
-    T* out = (UPDATE ? z : eps_out) + static_cast<uint64_t>(o0) * Dx;
-    // one run: bulk copy when 16-byte aligned (both ends), else cooperative
-    auto aligned = [](const void* g, uint32_t bytes) { return (reinterpret_cast<uintptr_t>(g) % 16 | bytes % 16) == 0; };
-    if (tid == 0) {
-        uint32_t tx = 0;
-        const uint32_t zb = rt * Dx * static_cast<uint32_t>(sizeof(T));
-        if (UPDATE && aligned(out, zb)) tx += zb;
-        for (int k = 0; k < p.n; ++k) {
-            const uint32_t len = static_cast<uint32_t>(p.e[k].len), b = rt * len * static_cast<uint32_t>(sizeof(T));
-            if (aligned(preds + p.e[k].base + static_cast<uint64_t>(o0) * len, b)) tx += b;
-        }
-        tc::mbar_arrive_expect_tx(&bar, tx);
-        if (UPDATE && aligned(out, zb)) tc::bulk_load(sm, out, zb, &bar);
-        for (int k = 0; k < p.n; ++k) {
-            const uint32_t len = static_cast<uint32_t>(p.e[k].len), b = rt * len * static_cast<uint32_t>(sizeof(T));
-            const T* src = preds + p.e[k].base + static_cast<uint64_t>(o0) * len;
-            if (aligned(src, b)) tc::bulk_load(sm + span_off[k], src, b, &bar);
-        }
-    }
-    {
-        const uint32_t zn = rt * Dx;
-        if (UPDATE && !aligned(out, zn * static_cast<uint32_t>(sizeof(T))))
-            for (uint32_t i = tid; i < zn; i += blockDim.x) sm[i] = out[i];
-        for (int k = 0; k < p.n; ++k) {
-            const uint32_t len = static_cast<uint32_t>(p.e[k].len), n = rt * len;
-            const T* src = preds + p.e[k].base + static_cast<uint64_t>(o0) * len;
-            if (!aligned(src, n * static_cast<uint32_t>(sizeof(T))))
-                for (uint32_t i = tid; i < n; i += blockDim.x) sm[span_off[k] + i] = src[i];
-        }
-    }
-    __syncthreads();
-    tc::mbar_wait(&bar, 0);
+    const uint32_t x = g % Dx, R = live / Dx;
     const CovLayout t(const_cast<void*>(table), static_cast<int>(Dx));
-    bool ok = true;
-    for (uint32_t q = warp; q < Dx; q += blockDim.x >> 5) {
-        const uint32_t x0 = __ldg(t.seg_x0 + q), w = __ldg(t.seg_w + q), c = __ldg(t.cnt + x0);
-        const uint32_t e = kWtRows * (q - x0) + lane;
-        const uint32_t row = e / w, x = x0 + (e - row * w);
-        if (row >= rt) continue;
-        double wv[kReconCover];
-        T r[kReconCover];
+    const uint32_t c = __ldg(t.cnt + x);
+    double w[CM];
+    float wf[CM];
+    bool has[CM];
+    uint32_t off[CM], str[CM];
 #pragma unroll
-        for (int cc = 0; cc < kReconCover; ++cc) {
-            wv[cc] = 0.0;
-            if (cc < static_cast<int>(c)) {
-                const int k = __ldg(t.kidx + cc * Dx + x0);  // uniform over the segment
-                const uint32_t len = static_cast<uint32_t>(p.e[k].len);
-                wv[cc] = __ldg(t.wts + cc * Dx + x);
-                r[cc] = sm[span_off[k] + row * len + (x - static_cast<uint32_t>(p.e[k].begin))];
+    for (int cc = 0; cc < CM; ++cc) {
+        has[cc] = cc < static_cast<int>(c);
+        const uint32_t sc = has[cc] ? cc : 0u;  // absent cover: cover 0's element (a valid address)
+        w[cc] = __ldg(t.wts + sc * Dx + x);
+        wf[cc] = static_cast<float>(w[cc]);
+        off[cc] = __ldg(t.offs + sc * Dx + x);
+        str[cc] = __ldg(t.ostr + sc * Dx + x);
+    }
+    const double Z = __ldg(t.zsum + x), Zi = __ldg(t.zinv + x);
+    const float Zf = __ldg(t.zsumf + x);
+    const bool z1 = FAST ? Zf == 1.f : Z == 1.0;
+    const bool mk = p.mk != 0;
+    bool ok = true;
+    constexpr int U = 4;
+    for (uint32_t o0 = g / Dx; o0 < rows; o0 += U * R) {
+        T raw[U][CM], zr[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t o = min(o0 + u * R, rows - 1);  // clamped: rows past the end are not stored
+#pragma unroll
+            for (int cc = 0; cc < CM; ++cc) raw[u][cc] = preds[off[cc] + static_cast<uint64_t>(o) * str[cc]];
+            if (UPDATE) zr[u] = z[static_cast<uint64_t>(o) * Dx + x];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t o = o0 + u * R;
+            double eps;
+            if (!FAST) {
+                double a = 0.0;  // from +0 like the reference's accumulator
+#pragma unroll
+                for (int cc = 0; cc < CM; ++cc) {
+                    const double s = __dadd_rn(a, __dmul_rn(w[cc], load_val<D>(raw[u], cc)));
+                    a = has[cc] ? s : a;
+                }
+                const double qd = mk ? div_z(a, Z, Zi) : __ddiv_rn(a, Z);
+                eps = quantize_dev<D>(z1 ? a : qd);
+            } else {
+                float a = 0.f;
+#pragma unroll
+                for (int cc = 0; cc < CM; ++cc) {
+                    const float s = fmaf(wf[cc], static_cast<float>(load_val<D>(raw[u], cc)), a);
+                    a = has[cc] ? s : a;
+                }
+                eps = quantize_dev<D>(static_cast<double>(z1 ? a : a / Zf));
+            }
+            bool fin = isfinite(eps);
+            double res = eps;
+            if (UPDATE) {
+                const double zo = load_val<D>(zr, u);
+                res = FAST ? static_cast<double>(fmaf(-static_cast<float>(p.eta), static_cast<float>(eps), static_cast<float>(zo)))
+                           : __dsub_rn(zo, __dmul_rn(p.eta, eps));
+            }
+            if (o < rows) {
+                T qv;
+                fin = store_q<D>(&qv, 0, res) && fin;
+                (UPDATE ? z : eps_out)[static_cast<uint64_t>(o) * Dx + x] = qv;
+                ok = ok && fin;
             }
         }
-        const double Z = __ldg(t.zsum + x), Zi = __ldg(t.zinv + x);
-        const float Zf = __ldg(t.zsumf + x);
-        T& cell = sm[row * Dx + x];
-        const T zraw = UPDATE ? cell : T{};
-        T qv;
-        const bool z1 = FAST ? Zf == 1.f : Z == 1.0;
-#define LP_K10W(CC)                                                                                     \
-    ok = (z1 ? k10_elem<D, UPDATE, FAST, CC, true>(wv, Z, Zi, Zf, p.mk, p.eta, r, zraw, qv)             \
-             : k10_elem<D, UPDATE, FAST, CC, false>(wv, Z, Zi, Zf, p.mk, p.eta, r, zraw, qv)) && ok;
-        switch (c) {
-            case 1: LP_K10W(1) break;
-            case 2: LP_K10W(2) break;
-            case 3: LP_K10W(3) break;
-            default: LP_K10W(4) break;
-        }
-#undef LP_K10W
-        cell = qv;
-    }
-    tc::fence_proxy_async();  // the generic-proxy writes above, before the bulk store reads them
-    __syncthreads();
-    const uint32_t ob = rt * Dx * static_cast<uint32_t>(sizeof(T));
-    if (aligned(out, ob)) {
-        if (tid == 0) {
-            tc::bulk_store(out, sm, ob);
-            tc::bulk_commit();
-            tc::bulk_wait_read<0>();  // shared memory must stay live until the store has read it
-        }
-    } else {
-        for (uint32_t i = tid; i < rt * Dx; i += blockDim.x) out[i] = sm[i];
     }
     if (!ok) raise_flag(LP_FLAG_NONFINITE);
 }
 
-// shared memory of k_reconstruct_wt for params p (0: not applicable)
-template <int D>
-static size_t recon_wt_smem(const ReconParams& p) {
-    const size_t al = 16 / D;
-    size_t elems = (kWtRows * static_cast<size_t>(p.D) + al - 1) / al * al;
-    for (int k = 0; k < p.n; ++k) elems += (kWtRows * static_cast<size_t>(p.e[k].len) + al - 1) / al * al;
-    const size_t bytes = elems * D + 128;
-    return bytes <= 160 * 1024 ? bytes : 0;
+// the largest number of entries covering one position of p's axis
+static int recon_max_cover(const ReconParams& p) {
+    int m = 0;
+    for (int64_t x = 0; x < p.D; ++x) {
+        int c = 0;
+        for (int k = 0; k < p.n; ++k) c += (x >= p.e[k].begin && x < p.e[k].begin + p.e[k].len);
+        m = std::max(m, c);
+    }
+    return m;
 }
 
 // Coverage-table K10 applicability: 32-bit offsets, total % 4 == 0, every position covered
@@ -1379,7 +1326,7 @@ static size_t recon_cov_bytes(const ReconParams& p, int dtype) {
     (void)dtype;
     if (p.n > 255) return 0;  // kidx is a byte
     const size_t bytes =
-        (static_cast<size_t>(p.D) * (kReconCover * 8 + 8 + 8 + 4 + kReconCover * 8 + 4 + 8 + kReconCover) + 15) / 16 * 16;
+        (static_cast<size_t>(p.D) * (kReconCover * 8 + 8 + 8 + 4 + kReconCover * 8 + 4 + kReconCover) + 15) / 16 * 16;
     return bytes <= 48 * 1024 ? bytes : 0;
 }
 
@@ -1459,20 +1406,27 @@ static void launch_recon(const ReconParams& p, const void* preds, void* z, void*
         auto* out_z = static_cast<T*>(z);
         auto* out_e = static_cast<T*>(eps);
         const auto* in = static_cast<const T*>(preds);
-        const size_t wt = p.inner == 1 && tune_get("recon_wt", 1) ? recon_wt_smem<D>(p) : 0;
-        if (wt) {
-            // W axis, tile form (knob recon_wt; 0 -> the x-stationary kernel below)
-            static size_t attr = 0;  // per <D, UPDATE> instantiation
-            if (attr < wt) {
-                LP_CUDA(cudaFuncSetAttribute(fast ? k_reconstruct_wt<D, UPDATE, true> : k_reconstruct_wt<D, UPDATE, false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wt)));
-                LP_CUDA(cudaFuncSetAttribute(fast ? k_reconstruct_wt<D, UPDATE, false> : k_reconstruct_wt<D, UPDATE, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wt)));
-                attr = wt;
+        const int cm = p.inner == 1 && tune_get("recon_xsb", 1) ? std::min(recon_max_cover(p), kReconCover) : 0;
+        if (cm > 0) {
+            // W axis, branch-free x-stationary form: threads in a multiple of D, one resident wave
+            auto pick = [&](auto kf) {
+                int rx = 0;
+                LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rx, kf, 256, 0));
+                const int64_t cap = static_cast<int64_t>(grid_for(INT32_MAX, 256, std::max(1, rx))) * 256;
+                const int64_t want = std::min<int64_t>(cap, p.total);
+                const uint32_t live = static_cast<uint32_t>(std::max<int64_t>(p.D, want / p.D * p.D));
+                kf<<<static_cast<int>((live + 255) / 256), 256, 0, st>>>(p, in, out_z, out_e, table, live);
+            };
+            switch (cm * 2 + (fast ? 1 : 0)) {
+                case 2: pick(k_reconstruct_xsb<D, UPDATE, false, 1>); break;
+                case 3: pick(k_reconstruct_xsb<D, UPDATE, true, 1>); break;
+                case 4: pick(k_reconstruct_xsb<D, UPDATE, false, 2>); break;
+                case 5: pick(k_reconstruct_xsb<D, UPDATE, true, 2>); break;
+                case 6: pick(k_reconstruct_xsb<D, UPDATE, false, 3>); break;
+                case 7: pick(k_reconstruct_xsb<D, UPDATE, true, 3>); break;
+                case 8: pick(k_reconstruct_xsb<D, UPDATE, false, 4>); break;
+                default: pick(k_reconstruct_xsb<D, UPDATE, true, 4>); break;
             }
-            const int gw = static_cast<int>((p.outer + kWtRows - 1) / kWtRows);
-            if (fast) k_reconstruct_wt<D, UPDATE, true><<<gw, 256, wt, st>>>(p, in, out_z, out_e, table);
-            else k_reconstruct_wt<D, UPDATE, false><<<gw, 256, wt, st>>>(p, in, out_z, out_e, table);
         } else if (p.inner == 1 && tune_get("recon_xs", 1)) {
             // x-stationary: threads in a multiple of D, one resident wave
             int rx = 0;

@@ -85,6 +85,31 @@ def test_attention_matches_torch(cuda, B, S, Skv, H):
     assert err <= 2e-2, err
 
 
+@pytest.mark.parametrize("B,S,H", [(1, 600, 1), (2, 1000, 3), (1, 1536, 2), (2, 1560, 12), (1, 130, 1)])
+def test_attention_cta_pair_matches_torch(cuda, B, S, H):
+    """Self-attention on CTA pairs (knob attn_pair: cta_group::2, K split by rows and V by
+    columns across the pair) vs torch fp32 SDPA, and vs the single-CTA kernel.  Shapes cover an
+    odd number of 256-row groups (the pair's second CTA past n_q), ragged key blocks and
+    n_kv not a multiple of 64 (the second CTA's keys partly out of range)."""
+    g = torch.Generator(device="cuda").manual_seed(S + 7 * H)
+    q = torch.randn(B, S, H, 128, device="cuda", generator=g).bfloat16()
+    k = torch.randn(B, S, H, 128, device="cuda", generator=g).bfloat16()
+    v = torch.randn(B, S, H, 128, device="cuda", generator=g).bfloat16()
+    scale = 1.0 / 128 ** 0.5
+    single = _attn(q, k, v, scale).float()
+    _lib.check(_lib.lib().lp_tune(b"attn_pair", 1))
+    try:
+        o = _attn(q, k, v, scale).float()
+        torch.cuda.synchronize()
+    finally:
+        _lib.check(_lib.lib().lp_tune(b"attn_pair", 0))
+    ref = torch.nn.functional.scaled_dot_product_attention(q.float().transpose(1, 2), k.float().transpose(1, 2),
+                                                           v.float().transpose(1, 2)).transpose(1, 2)
+    assert (o - ref).abs().max().item() <= 2e-2
+    # same arithmetic per row as the single-CTA kernel: identical up to MMA accumulation order
+    assert (o - single).abs().max().item() <= 1e-2
+
+
 def test_attention_large_logits(cuda):
     # scores far from 0 exercise the lazy-rescale path (max jumps by > 8 in log2 units)
     g = torch.Generator(device="cuda").manual_seed(5)

@@ -198,6 +198,12 @@ def test_nonfinite_is_reported(cuda):
         zt = lp.LatentTensor(torch.zeros(dims, dtype=dt, device="cuda"), d)
         eps = lp.LatentTensor(torch.zeros(dims, dtype=dt, device="cuda"), d)
         eps.data[1, 0, 0, 0] = float("inf")
+        out = lp.sampler_step(zt, eps, 1, 0.05)
+        if d == 4:  # the reference's F32 quantize saturates -inf to -FLT_MAX (src/dtype.cpp:106-111)
+            assert lp.device_flags() == 0 and out.to_numpy()[1, 0, 0, 0] == -np.finfo(np.float32).max
+        else:
+            assert lp.device_flags() & 1, d
+        eps.data[1, 0, 0, 0] = float("nan")  # NaN survives every quantize
         lp.sampler_step(zt, eps, 1, 0.05)
         assert lp.device_flags() & 1, d
         assert lp.device_flags() == 0  # reset by the read
@@ -255,11 +261,12 @@ def test_reconstruct_paths_bitexact(cuda, oracle, shape, patch, k, r, step, d):
     ((1, 3, 3, 40), 8, 1.0),       # 9 rows (< one tile), 8 workers, up to 3 covers per position
     ((16, 21, 60, 104), 4, 0.5),   # C2's W axis
 ])
-@pytest.mark.parametrize("wt", [1, 0])
-def test_reconstruct_w_axis_tile_bitexact(cuda, oracle, shape, k, r, d, wt):
-    """K10 on W-axis plans (inner == 1): the tile kernel k_reconstruct_wt (knob recon_wt=1, bulk
-    copies of 32-row runs, segment-uniform warps) and the x-stationary kernel (recon_wt=0),
-    exact mode, reconstruct and fused update, bit for bit against the oracle."""
+@pytest.mark.parametrize("xsb", [1, 0])
+def test_reconstruct_w_axis_bitexact(cuda, oracle, shape, k, r, d, xsb):
+    """K10 on W-axis plans (inner == 1): the branch-free x-stationary kernel k_reconstruct_xsb
+    (knob recon_xsb=1: every lane evaluates the plan's maximum cover count, absent covers
+    dropped by selects) and the branching one (recon_xsb=0), exact mode, reconstruct and fused
+    update, bit for bit vs the oracle."""
     from paper_2512_07350_b200 import _lib
 
     patch = (1, 1, 1) if shape[3] % 2 else (1, 2, 2)
@@ -272,11 +279,11 @@ def test_reconstruct_w_axis_tile_bitexact(cuda, oracle, shape, k, r, d, wt):
                 for e in range(oplan.n)]
     want = oracle.reconstruct(np.concatenate([p.reshape(-1) for p in preds_np]), shape, d, oplan)
     preds = [lp.LatentTensor.from_numpy(p, d) for p in preds_np]
-    _lib.check(_lib.lib().lp_tune(b"recon_wt", wt))
+    _lib.check(_lib.lib().lp_tune(b"recon_xsb", xsb))
     try:
         assert np.array_equal(lp.reconstruct(preds, plan, shape).to_numpy(), want)
         zt = lp.LatentTensor.from_numpy(z, d)
         lp.reconstruct_update(preds, plan, zt, 0.05)
         assert np.array_equal(zt.to_numpy(), oracle.sampler_step(z, want, d, 0.05))
     finally:
-        _lib.check(_lib.lib().lp_tune(b"recon_wt", 1))
+        _lib.check(_lib.lib().lp_tune(b"recon_xsb", 1))

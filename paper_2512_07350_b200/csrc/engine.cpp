@@ -753,24 +753,48 @@ int lp_engine_hbm_bench(lp_engine* e, int32_t step, int32_t iters, int32_t sets,
         }
         cudaEvent_t ev[3] = {};
         for (auto& x : ev) LP_CUDA(cudaEventCreate(&x));
-        auto k1 = [&](int s) {
+        auto k1 = [&](int s, cudaStream_t q) {
             if (!L.owned.empty())
-                gather_entries(zp(s), e->shape, plan, L.owned.data(), static_cast<int>(L.owned.size()), E, zp(s) + zs, st);
+                gather_entries(zp(s), e->shape, plan, L.owned.data(), static_cast<int>(L.owned.size()), E, zp(s) + zs, q);
         };
-        auto k10 = [&](int s) {
-            reconstruct_dispatch(e->recon[a], E, zp(s) + zs + ss, zp(s), nullptr, true, c.mode == LP_MODE_FAST, st);
+        auto k10 = [&](int s, cudaStream_t q) {
+            reconstruct_dispatch(e->recon[a], E, zp(s) + zs + ss, zp(s), nullptr, true, c.mode == LP_MODE_FAST, q);
         };
-        for (int s = 0; s < sets; ++s) { k1(s); k10(s); }  // warm-up (and K10's coverage table)
+        for (int s = 0; s < sets; ++s) { k1(s, st); k10(s, st); }  // warm-up (and K10's coverage table)
+        LP_CUDA(cudaStreamSynchronize(st));
+        // each loop of `iters` launches replays as ONE CUDA graph: no host launch gaps between
+        // these few-us kernels (eager launches from the host loop would time the launch rate)
+        cudaStream_t cs = nullptr;
+        LP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        const bool prof = prof_enabled();
+        if (prof) lp_profile_enable(0);  // no profiling events inside the captured loops
+        auto capture = [&](auto body) {
+            cudaGraph_t g = nullptr;
+            cudaGraphExec_t x = nullptr;
+            LP_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            for (int it = 0; it < iters; ++it) body(it % sets, cs);
+            LP_CUDA(cudaStreamEndCapture(cs, &g));
+            LP_CUDA(cudaGraphInstantiate(&x, g, 0));
+            cudaGraphDestroy(g);
+            return x;
+        };
+        cudaGraphExec_t g1 = capture(k1), g10 = capture(k10);
+        if (prof) lp_profile_enable(1);
+        LP_CUDA(cudaGraphLaunch(g1, st));  // graph warm-up
+        LP_CUDA(cudaGraphLaunch(g10, st));
         LP_CUDA(cudaEventRecord(ev[0], st));
-        for (int it = 0; it < iters; ++it) k1(it % sets);
+        LP_CUDA(cudaGraphLaunch(g1, st));
         LP_CUDA(cudaEventRecord(ev[1], st));
-        for (int it = 0; it < iters; ++it) k10(it % sets);
+        LP_CUDA(cudaGraphLaunch(g10, st));
         LP_CUDA(cudaEventRecord(ev[2], st));
         LP_CUDA(cudaEventSynchronize(ev[2]));
         float m1 = 0.f, m2 = 0.f;
         LP_CUDA(cudaEventElapsedTime(&m1, ev[0], ev[1]));
         LP_CUDA(cudaEventElapsedTime(&m2, ev[1], ev[2]));
         for (auto& x : ev) cudaEventDestroy(x);
+        cudaGraphExecDestroy(g1);
+        cudaGraphExecDestroy(g10);
+        cudaStreamDestroy(cs);
         LP_CUDA(cudaFree(buf));
         out[0] = static_cast<double>(m1) / iters;
         out[1] = 2.0 * static_cast<double>(subb);                // K1: read the windows, write them packed

@@ -371,8 +371,14 @@ __device__ __forceinline__ void epi_chunk_smem(const GemmEpilogue& ep, int col0,
         }
         if (ep.xq) {
             // LayerNorm partials of this chunk's 32 values, merged into the tile's (lnfold.cuh)
+#ifndef LP_LNFOLD_NOMERGE  // A/B builds only (wrong results): the cost of the partials / xq stores
             ln_chunk_merge(v, chunk, ln.st_mean, ln.st_m2);
+#endif
+#ifdef LP_LNFOLD_NOXQ
+            if (false) {
+#else
             if (ln.xq) {
+#endif
                 uint4* o = reinterpret_cast<uint4*>(ln.xq + col0);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {

@@ -8,7 +8,6 @@
 #include <cuda_bf16.h>
 
 #include "dit_kernels.hpp"
-#include "lnfold.cuh"
 
 namespace lpb200 {
 
@@ -272,35 +271,6 @@ void lnfold_vectors(const LnFoldJob* jobs_dev, int njobs, int max_n, cudaStream_
 
 // One thread per (row, part): the part's columns in 32-value chunks, through the same
 // operations as the GEMM producer epilogue (lnfold.cuh), so the partials are bit-identical.
-__global__ void __launch_bounds__(256) k_ln_stats_xq(const float* __restrict__ x, __nv_bfloat16* __restrict__ xq,
-                                                     float2* __restrict__ stats, int64_t rows, int d,
-                                                     const float* __restrict__ g, int plus1, int parts) {
-    const int64_t i = blockIdx.x * 256LL + threadIdx.x;
-    if (i >= rows * parts) return;
-    const int64_t row = i / parts;
-    const int part = static_cast<int>(i - row * parts), w = d / parts;
-    float mean = 0.f, m2 = 0.f;
-    for (int c = 0; c < w / 32; ++c) {
-        const int col0 = part * w + 32 * c;
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(v + j) = *reinterpret_cast<const float4*>(x + row * d + col0 + j);
-        ln_chunk_merge(v, c, mean, m2);
-        uint4* o = reinterpret_cast<uint4*>(xq + row * d + col0);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) o[j] = ln_xq8(v + 8 * j, g + col0 + 8 * j, plus1);
-    }
-    stats[i] = make_float2(mean, m2);
-}
-
-void ln_stats_xq(const float* x, __nv_bfloat16* xq, float2* stats, int64_t rows, int d, const float* g, bool plus1,
-                 int parts, cudaStream_t st) {
-    if (parts < 1 || d % parts || (d / parts) % 32) fail(LP_ERR_INVALID_ARGUMENT, "ln_stats_xq: parts must split d into 32-column chunks");
-    const int64_t n = rows * parts;
-    k_ln_stats_xq<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(x, xq, stats, rows, d, g, plus1 ? 1 : 0, parts);
-    LP_LAUNCH_CHECK();
-}
 
 // ---------------------------------------------------------------------------
 // RMSNorm over the full width d of a [rows, ld] bf16 slice (cols [col0, col0+d)),

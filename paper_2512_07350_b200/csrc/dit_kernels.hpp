@@ -42,11 +42,6 @@ struct LnFoldJob {
     int N, K, plus1, pad;
 };
 void lnfold_vectors(const LnFoldJob* jobs_dev, int njobs, int max_n, cudaStream_t st);
-// The producer half of the fold for a residual stream x no GEMM epilogue wrote (a pipeline
-// stage's input): xq = bf16(x * g) (plus1: x * (1 + g)), and `parts` LayerNorm partials per
-// row, bit-identical to what the GEMM producer epilogue writes (lnfold.cuh).
-void ln_stats_xq(const float* x, __nv_bfloat16* xq, float2* stats, int64_t rows, int d, const float* g, bool plus1,
-                 int parts, cudaStream_t st);
 void rmsnorm_rope(__nv_bfloat16* buf, int64_t rows, int64_t ld, int64_t col0, int d, const float* g, float eps,
                   bool rope, int64_t rows_per_batch, int nh, int nw, cudaStream_t st);
 // RoPE cos/sin table [nf*22 + nh*21 + nw*21] float2 of a shard grid (once per forward).

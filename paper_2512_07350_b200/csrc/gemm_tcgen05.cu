@@ -309,13 +309,12 @@ __device__ __forceinline__ void tma_load_2d_cta(const void* tmap, uint64_t* bar,
 // Per-row LayerNorm state of the LN-fold epilogue (one lane = one row of the tile).
 struct LnRow {
     float mean = 0.f, rstd = 1.f;  // consumer: the row's LayerNorm statistics
-    float st_mean = 0.f, st_m2 = 0.f;  // producer: running partials over this tile's chunks
-    __nv_bfloat16* xq = nullptr;  // producer: this row's xq (null: row >= M or off)
+    LnAcc acc;                    // producer: partials over this tile's chunks
 };
 
-template <int MODE>
+template <int MODE, bool XQ = false>
 __device__ __forceinline__ void epi_chunk_smem(const GemmEpilogue& ep, int col0, const uint32_t (&r)[32], uint8_t* box,
-                                               LnRow& ln, int chunk) {
+                                               LnRow& ln, int chunk, uint8_t* xqbox = nullptr) {
     const uint32_t lane = lane_id();
     float v[32];
 #pragma unroll
@@ -369,24 +368,18 @@ __device__ __forceinline__ void epi_chunk_smem(const GemmEpilogue& ep, int col0,
             v[4 * j + 2] = x.z;
             v[4 * j + 3] = x.w;
         }
-        if (ep.xq) {
-            // LayerNorm partials of this chunk's 32 values, merged into the tile's (lnfold.cuh)
-#ifndef LP_LNFOLD_NOMERGE  // A/B builds only (wrong results): the cost of the partials / xq stores
-            ln_chunk_merge(v, chunk, ln.st_mean, ln.st_m2);
-#endif
-#ifdef LP_LNFOLD_NOXQ
-            if (false) {
-#else
-            if (ln.xq) {
-#endif
-                uint4* o = reinterpret_cast<uint4*>(ln.xq + col0);
+        if (XQ) {
+            // LayerNorm partials of this chunk's 32 values (lnfold.cuh), and xq = bf16(x * g)
+            // into this chunk's 32 x 32 bf16 staging box (64-byte rows, the bf16 output layout),
+            // TMA-stored by the caller next to the x box
+            ln_acc_chunk(v, chunk, ln.acc);
+            uint8_t* row = xqbox + lane * 64;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    float g[8];
-                    *reinterpret_cast<float4*>(g) = __ldg(reinterpret_cast<const float4*>(ep.g + col0 + 8 * j));
-                    *reinterpret_cast<float4*>(g + 4) = __ldg(reinterpret_cast<const float4*>(ep.g + col0 + 8 * j + 4));
-                    o[j] = ln_xq8(v + 8 * j, g, ep.g_plus1);
-                }
+            for (int j = 0; j < 4; ++j) {
+                float g[8];
+                *reinterpret_cast<float4*>(g) = __ldg(reinterpret_cast<const float4*>(ep.g + col0 + 8 * j));
+                *reinterpret_cast<float4*>(g + 4) = __ldg(reinterpret_cast<const float4*>(ep.g + col0 + 8 * j + 4));
+                *reinterpret_cast<uint4*>(row + ((j ^ ((lane >> 1) & 3)) << 4)) = ln_xq8(v + 8 * j, g, ep.g_plus1);
             }
         }
     }
@@ -409,19 +402,25 @@ __device__ __forceinline__ void epi_chunk_smem(const GemmEpilogue& ep, int col0,
 #endif
 template <int MODE>
 constexpr int epi_boxes() { return kEpiTma ? (MODE == EPI_F32_RESID ? LP_EPI_RESID_BOXES : 2) : 0; }
-template <int BN, int MODE = EPI_BF16>
-constexpr int gemm2_stages() { return (BN == 256 ? 6 : 8) - (epi_boxes<MODE>() > 2 ? (BN == 256 ? 1 : 2) : 0); }
-template <int BN, int MODE>
+// XQ (LayerNorm-fold producer): two extra 2 KB bf16 boxes per epilogue warp for xq, paid for
+// with one mainloop stage
+constexpr int kXqBox = 2048;
+template <int BN, int MODE = EPI_BF16, bool XQ = false>
+constexpr int gemm2_stages() {
+    return (BN == 256 ? 6 : 8) - (epi_boxes<MODE>() > 2 ? (BN == 256 ? 1 : 2) : 0) - (XQ ? 1 : 0);
+}
+template <int BN, int MODE, bool XQ = false>
 constexpr int gemm2_smem_bytes() {
-    return gemm2_stages<BN, MODE>() * (kBM * kBK * 2 + (BN / 2) * kBK * 2) + 1024 + 512 +
-           4 * epi_boxes<MODE>() * kEpiBox;
+    return gemm2_stages<BN, MODE, XQ>() * (kBM * kBK * 2 + (BN / 2) * kBK * 2) + 1024 + 512 +
+           4 * epi_boxes<MODE>() * kEpiBox + (XQ ? 4 * 2 * kXqBox : 0);
 }
 
-template <int BN, int MODE>
+template <int BN, int MODE, bool XQ = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
-            const __grid_constant__ CUtensorMap tmo, GemmEpilogue ep, int M, int N, int K) {
-    constexpr int S = gemm2_stages<BN, MODE>();
+            const __grid_constant__ CUtensorMap tmo, const __grid_constant__ CUtensorMap tmq, GemmEpilogue ep, int M,
+            int N, int K) {
+    constexpr int S = gemm2_stages<BN, MODE, XQ>();
     constexpr int NB = epi_boxes<MODE>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -429,7 +428,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint8_t* sA = smem;
     uint8_t* sB = smem + S * A_BYTES;
     uint8_t* sE = sB + S * B_BYTES;  // [4 epilogue warps][NB][kEpiBox] (1024-aligned)
-    uint64_t* full = reinterpret_cast<uint64_t*>(sE + 4 * NB * kEpiBox);
+    uint8_t* sX = sE + 4 * NB * kEpiBox;  // [4 epilogue warps][2][kXqBox] (XQ)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sX + (XQ ? 4 * 2 * kXqBox : 0));
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
@@ -570,7 +570,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 ln.mean = mean;
                 ln.rstd = rsqrtf(m2 / (ep.cols_per_part * static_cast<float>(ep.parts)) + ep.eps);
             }
-            if (MODE >= EPI_F32_RESID && ep.xq && my_row < M) ln.xq = ep.xq + static_cast<int64_t>(my_row) * ep.ldq;
 #pragma unroll 1
             for (int c = 0; c < NCH; ++c, ++u) {
                 const int b = u % NB;
@@ -583,18 +582,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 } else if (lane == 0) {
                     bulk_wait_read<1>();  // the store issued from this buffer two chunks ago has read it
                 }
+                // XQ: xq box u % 2 was last stored at chunk u - 2 (issue_next waits for that
+                // except at the very tail, where it issues no load)
+                if (XQ && RESID && lane == 0) bulk_wait_read<1>();
                 __syncwarp();
                 tmem_ld_wait();
-                epi_chunk_smem<MODE>(ep, nb * BN + c * 32, r, boxes + b * kEpiBox, ln, c);
+                // xq box u % 2: its last store (chunk u - 2) has been read — the wait above
+                // leaves at most one store group (chunk u - 1) in flight
+                uint8_t* xqb = sX + (q * 2 + (u & 1)) * kXqBox;
+                epi_chunk_smem<MODE, XQ>(ep, nb * BN + c * 32, r, boxes + b * kEpiBox, ln, c, xqb);
                 fence_proxy_async();
                 __syncwarp();
                 if (lane == 0) {
                     tma_store_2d(&tmo, boxes + b * kEpiBox, nb * BN + c * 32, row0);
+                    if (XQ) tma_store_2d(&tmq, xqb, nb * BN + c * 32, row0);
                     bulk_commit();
                 }
             }
-            if (MODE >= EPI_F32_RESID && ep.stats_out && my_row < M)
-                ep.stats_out[static_cast<int64_t>(my_row) * num_n + nb] = make_float2(ln.st_mean, ln.st_m2);
+            if (XQ && my_row < M)
+                ep.stats_out[static_cast<int64_t>(my_row) * num_n + nb] = ln_acc_final(ln.acc, static_cast<float>(BN));
             tc_fence_before();
             mbar_arrive_cluster(&tempty[acc], 0);
         }
@@ -655,21 +661,35 @@ static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Gemm
     LP_LAUNCH_CHECK();
 }
 
+template <int BN, int MODE, bool XQ>
+static void launch_gemm2_x(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& tq,
+                           const GemmEpilogue& ep, int M, int N, int K, cudaStream_t st) {
+    constexpr int smem = gemm2_smem_bytes<BN, MODE, XQ>();
+    static bool attr = false;
+    if (!attr) {
+        LP_CUDA(cudaFuncSetAttribute(k_gemm2<BN, MODE, XQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * (N / BN);
+    const int clusters = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+    k_gemm2<BN, MODE, XQ><<<2 * clusters, kGemmThreads, smem, st>>>(ta, tb, to, tq, ep, M, N, K);
+    LP_LAUNCH_CHECK();
+}
+
 template <int BN, int MODE>
 static void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmEpilogue& ep, int M, int N, int K,
                          cudaStream_t st) {
     const CUtensorMap to = make_tmap_epi(ep.out, MODE >= EPI_F32_RESID, static_cast<uint64_t>(N), static_cast<uint64_t>(M),
                                          static_cast<uint64_t>(ep.ldo));
-    constexpr int smem = gemm2_smem_bytes<BN, MODE>();
-    static bool attr = false;
-    if (!attr) {
-        LP_CUDA(cudaFuncSetAttribute(k_gemm2<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
+    if constexpr (MODE >= EPI_F32_RESID && kEpiTma) {
+        if (ep.xq) {  // LayerNorm-fold producer: xq (bf16, 32 x 32 boxes) stored by TMA next to x
+            const CUtensorMap tq = make_tmap_epi(ep.xq, false, static_cast<uint64_t>(N), static_cast<uint64_t>(M),
+                                                 static_cast<uint64_t>(ep.ldq));
+            launch_gemm2_x<BN, MODE, true>(ta, tb, to, tq, ep, M, N, K, st);
+            return;
+        }
     }
-    const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * (N / BN);
-    const int clusters = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-    k_gemm2<BN, MODE><<<2 * clusters, kGemmThreads, smem, st>>>(ta, tb, to, ep, M, N, K);
-    LP_LAUNCH_CHECK();
+    launch_gemm2_x<BN, MODE, false>(ta, tb, to, to, ep, M, N, K, st);
 }
 
 static int gemm_variant() { return tune_get("gemm_2sm", 1); }

@@ -1,29 +1,35 @@
-// lnfold.cuh — the LayerNorm-fold producer arithmetic shared by the GEMM epilogue
-// (gemm_tcgen05.cu) and the stage-boundary pass (dit_kernels.cu), written with explicit
-// round-to-nearest intrinsics so both compile to the same operations: a pipeline stage that
-// recomputes the partials from x gets the bits the GEMM epilogue would have written.
+// lnfold.cuh — the LayerNorm-fold producer arithmetic of the GEMM epilogue (gemm_tcgen05.cu,
+// knob dit_lnfold), written with explicit round-to-nearest intrinsics (no contraction).
 #pragma once
 
 #include <cuda_bf16.h>
 
 namespace lpb200 {
 
-// Merge the LayerNorm partials of one 32-value chunk (the chunk-th of its tile, counted from
-// 0) into the tile's running (mean, M2) (Chan et al.; equal chunk sizes).
-__device__ __forceinline__ void ln_chunk_merge(const float (&v)[32], int chunk, float& mean, float& m2) {
-    float m = 0.f;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) m = __fadd_rn(m, v[j]);
-    m = __fmul_rn(m, 1.f / 32.f);
-    float c2 = 0.f;
+// LayerNorm partials of one part (a GEMM tile's columns), fed
+// 32-value chunks in column order.  Shifted sums: K = the part's first value, then four
+// independent (Σd, Σd²) accumulators over d = v - K (chain length 8 per chunk instead of a 32-deep
+// serial Welford/Chan merge, which cost the residual GEMM epilogues ~4% of the step, r3k).  The
+// shift keeps Σd² - (Σd)²/n well conditioned (K is within a few standard deviations of the mean).
+struct LnAcc {
+    float k = 0.f;
+    float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+};
+__device__ __forceinline__ void ln_acc_chunk(const float (&v)[32], int chunk, LnAcc& a) {
+    if (chunk == 0) a.k = v[0];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-        const float dlt = __fsub_rn(v[j], m);
-        c2 = __fmaf_rn(dlt, dlt, c2);
+        const float d = __fsub_rn(v[j], a.k);
+        a.s1[j & 3] = __fadd_rn(a.s1[j & 3], d);
+        a.s2[j & 3] = __fmaf_rn(d, d, a.s2[j & 3]);
     }
-    const float dlt = __fsub_rn(m, mean), inv = __frcp_rn(static_cast<float>(chunk + 1));
-    mean = __fmaf_rn(dlt, inv, mean);
-    m2 = __fadd_rn(m2, __fmaf_rn(__fmul_rn(dlt, dlt), __fmul_rn(32.f * static_cast<float>(chunk), inv), c2));
+}
+// (mean, M2) of the part's n values, the form the consumer merges across parts
+__device__ __forceinline__ float2 ln_acc_final(const LnAcc& a, float n) {
+    const float S1 = __fadd_rn(__fadd_rn(a.s1[0], a.s1[1]), __fadd_rn(a.s1[2], a.s1[3]));
+    const float S2 = __fadd_rn(__fadd_rn(a.s2[0], a.s2[1]), __fadd_rn(a.s2[2], a.s2[3]));
+    const float m = __fdiv_rn(S1, n);
+    return make_float2(__fadd_rn(a.k, m), fmaxf(__fmaf_rn(-S1, m, S2), 0.f));
 }
 
 // xq = bf16(x * g) (plus1: x * (1 + g)) for 8 consecutive values, packed

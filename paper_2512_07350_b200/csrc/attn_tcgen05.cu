@@ -206,8 +206,14 @@ __device__ __forceinline__ void softmax_block(uint32_t tS, uint32_t tO, int vali
     auto publish = [&](uint64_t* bar, int half) {
         tmem_st_wait();
         tc_fence_before();
-        if (PAIR) mbar_arrive_cluster(bar, 0);  // CTA pair: the leader's barrier counts both CTAs' rows
-        else mbar_arrive(bar);
+        if (PAIR) {
+            // CTA pair: one remote arrive per warp on the leader's barrier (count 8 = 4 warps x
+            // 2 CTAs) once all 32 lanes' TMEM stores are complete
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(bar, 0);
+        } else {
+            mbar_arrive(bar);
+        }
         if (tr0) trace_ev<TR>(j, t, 2 + half);
         // per lane-quarter arrival (events 8..11 p_half, 12..15 p_full): the barrier completes
         // at the slowest of the four warps
@@ -563,7 +569,7 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
 // the tensor core reads from it (S: 64 -> 48 KB per tile, PV: 32 -> 16 KB), and one issued
 // MMA covers both SMs.  Barriers: Q/K/V completions count both CTAs' bytes on the leader's
 // barriers (2-SM TMA), the leader's commits are multicast to both CTAs (s_full, k/v_empty,
-// o_final), and both CTAs' softmax rows arrive on the leader's p_half / p_full (count 256).
+// o_final), and both CTAs' softmax warps arrive on the leader's p_half / p_full (count 8).
 // The softmax and epilogue are the single-CTA kernel's.
 // ---------------------------------------------------------------------------
 constexpr int kPairKS = 4, kPairVS = 4;
@@ -622,8 +628,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAttnThreads, 1)
         }
         for (int t = 0; t < NT; ++t) {
             mbar_init(&s_full[t], 1);
-            mbar_init(&p_full[t], 256);
-            mbar_init(&p_half[t], 256);
+            mbar_init(&p_full[t], 8);
+            mbar_init(&p_half[t], 8);
             mbar_init(&o_final[t], 1);
         }
         fence_barrier_init();

@@ -1218,7 +1218,7 @@ __global__ void __launch_bounds__(256) k_reconstruct_xs(const __grid_constant__ 
 // dropped by a select, so the worker-order sum is the reference's bit for bit, NaN / inf
 // included; the division and the Z == 1 shortcut are both evaluated and selected.  No branch
 // depends on x.
-template <int D, bool UPDATE, bool FAST, int CM>
+template <int D, bool UPDATE, bool FAST, int CM, int U = 4>
 __global__ void __launch_bounds__(256) k_reconstruct_xsb(const __grid_constant__ ReconParams p,
                                                          const typename Store<D>::T* __restrict__ preds,
                                                          typename Store<D>::T* __restrict__ z,
@@ -1250,7 +1250,6 @@ __global__ void __launch_bounds__(256) k_reconstruct_xsb(const __grid_constant__
     const bool z1 = FAST ? Zf == 1.f : Z == 1.0;
     const bool mk = p.mk != 0;
     bool ok = true;
-    constexpr int U = 4;
     for (uint32_t o0 = g / Dx; o0 < rows; o0 += U * R) {
         T raw[U][CM], zr[U];
 #pragma unroll
@@ -1417,15 +1416,17 @@ static void launch_recon(const ReconParams& p, const void* preds, void* z, void*
                 const uint32_t live = static_cast<uint32_t>(std::max<int64_t>(p.D, want / p.D * p.D));
                 kf<<<static_cast<int>((live + 255) / 256), 256, 0, st>>>(p, in, out_z, out_e, table, live);
             };
+            // rows in flight per thread (knob recon_u: 4 or 8)
+            const bool u8 = tune_get("recon_u", 4) == 8;
             switch (cm * 2 + (fast ? 1 : 0)) {
-                case 2: pick(k_reconstruct_xsb<D, UPDATE, false, 1>); break;
-                case 3: pick(k_reconstruct_xsb<D, UPDATE, true, 1>); break;
-                case 4: pick(k_reconstruct_xsb<D, UPDATE, false, 2>); break;
-                case 5: pick(k_reconstruct_xsb<D, UPDATE, true, 2>); break;
-                case 6: pick(k_reconstruct_xsb<D, UPDATE, false, 3>); break;
-                case 7: pick(k_reconstruct_xsb<D, UPDATE, true, 3>); break;
-                case 8: pick(k_reconstruct_xsb<D, UPDATE, false, 4>); break;
-                default: pick(k_reconstruct_xsb<D, UPDATE, true, 4>); break;
+                case 2: u8 ? pick(k_reconstruct_xsb<D, UPDATE, false, 1, 8>) : pick(k_reconstruct_xsb<D, UPDATE, false, 1>); break;
+                case 3: u8 ? pick(k_reconstruct_xsb<D, UPDATE, true, 1, 8>) : pick(k_reconstruct_xsb<D, UPDATE, true, 1>); break;
+                case 4: u8 ? pick(k_reconstruct_xsb<D, UPDATE, false, 2, 8>) : pick(k_reconstruct_xsb<D, UPDATE, false, 2>); break;
+                case 5: u8 ? pick(k_reconstruct_xsb<D, UPDATE, true, 2, 8>) : pick(k_reconstruct_xsb<D, UPDATE, true, 2>); break;
+                case 6: u8 ? pick(k_reconstruct_xsb<D, UPDATE, false, 3, 8>) : pick(k_reconstruct_xsb<D, UPDATE, false, 3>); break;
+                case 7: u8 ? pick(k_reconstruct_xsb<D, UPDATE, true, 3, 8>) : pick(k_reconstruct_xsb<D, UPDATE, true, 3>); break;
+                case 8: u8 ? pick(k_reconstruct_xsb<D, UPDATE, false, 4, 8>) : pick(k_reconstruct_xsb<D, UPDATE, false, 4>); break;
+                default: u8 ? pick(k_reconstruct_xsb<D, UPDATE, true, 4, 8>) : pick(k_reconstruct_xsb<D, UPDATE, true, 4>); break;
             }
         } else if (p.inner == 1 && tune_get("recon_xs", 1)) {
             // x-stationary: threads in a multiple of D, one resident wave

@@ -261,12 +261,12 @@ def test_reconstruct_paths_bitexact(cuda, oracle, shape, patch, k, r, step, d):
     ((1, 3, 3, 40), 8, 1.0),       # 9 rows (< one tile), 8 workers, up to 3 covers per position
     ((16, 21, 60, 104), 4, 0.5),   # C2's W axis
 ])
-@pytest.mark.parametrize("xsb", [1, 0])
-def test_reconstruct_w_axis_bitexact(cuda, oracle, shape, k, r, d, xsb):
+@pytest.mark.parametrize("xsb,u", [(1, 4), (1, 8), (0, 4)])
+def test_reconstruct_w_axis_bitexact(cuda, oracle, shape, k, r, d, xsb, u):
     """K10 on W-axis plans (inner == 1): the branch-free x-stationary kernel k_reconstruct_xsb
     (knob recon_xsb=1: every lane evaluates the plan's maximum cover count, absent covers
-    dropped by selects) and the branching one (recon_xsb=0), exact mode, reconstruct and fused
-    update, bit for bit vs the oracle."""
+    dropped by selects; 4 or 8 rows in flight, knob recon_u) and the branching one
+    (recon_xsb=0), exact mode, reconstruct and fused update, bit for bit vs the oracle."""
     from paper_2512_07350_b200 import _lib
 
     patch = (1, 1, 1) if shape[3] % 2 else (1, 2, 2)
@@ -280,6 +280,7 @@ def test_reconstruct_w_axis_bitexact(cuda, oracle, shape, k, r, d, xsb):
     want = oracle.reconstruct(np.concatenate([p.reshape(-1) for p in preds_np]), shape, d, oplan)
     preds = [lp.LatentTensor.from_numpy(p, d) for p in preds_np]
     _lib.check(_lib.lib().lp_tune(b"recon_xsb", xsb))
+    _lib.check(_lib.lib().lp_tune(b"recon_u", u))
     try:
         assert np.array_equal(lp.reconstruct(preds, plan, shape).to_numpy(), want)
         zt = lp.LatentTensor.from_numpy(z, d)
@@ -287,3 +288,4 @@ def test_reconstruct_w_axis_bitexact(cuda, oracle, shape, k, r, d, xsb):
         assert np.array_equal(zt.to_numpy(), oracle.sampler_step(z, want, d, 0.05))
     finally:
         _lib.check(_lib.lib().lp_tune(b"recon_xsb", 1))
+        _lib.check(_lib.lib().lp_tune(b"recon_u", 4))

@@ -178,7 +178,6 @@ __device__ __forceinline__ void softmax_block(uint32_t tS, uint32_t tO, int vali
     if (need) m_run = mx;
     const float2 c2 = make_float2(c, c), nmc2 = make_float2(-m_run * c, -m_run * c);
     float2 lsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
     // 32-column chunks, the next chunk's TMEM load in flight while this one is computed
     // (register double buffer; LDTM results are scoreboard-tracked)
     auto chunk = [&](const uint32_t (&r)[32], int cc) {

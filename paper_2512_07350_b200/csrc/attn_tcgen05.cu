@@ -65,6 +65,7 @@ struct AttnKernelArgs {
     int64_t ldo;
     float scale_log2;  // softmax scale * log2(e)
     int heads, batch;
+    int p_whole;  // MMA warp: wait for the whole P (p_full) before any PV instead of half by half
 };
 
 #ifndef LP_ATTN_MAX2
@@ -430,16 +431,20 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
                 const bool more = j + 1 < nkv;
                 const uint32_t g = g0 + static_cast<uint32_t>(j);
                 for (int t = 0; t < NT; ++t) {
-                    wait1(&p_half[t], (g & 1u));
+                    // knob attn_pwhole: one barrier check per tile and block instead of two (every
+                    // check is a tensor-pipe bubble: the issue is nearly synchronous)
+                    wait1(a.p_whole ? &p_full[t] : &p_half[t], (g & 1u));
                     if (t == 0) wait1(&v_full[g % VS], ((g / VS) & 1u));
                     // O_t is overwritten by this item's first PV: the previous epilogue read it
                     if (j == 0 && it > 0) wait1(&o_empty[t], (it - 1) & 1);
                     if (lane == 0) trace_ev<TR>(j, t, 4);
                     tc_fence_after();
                     issue_pv(t, j, 0);
-                    wait1(&p_full[t], (g & 1u));
-                    if (lane == 0) trace_ev<TR>(j, t, 5);
-                    tc_fence_after();
+                    if (!a.p_whole) {
+                        wait1(&p_full[t], (g & 1u));
+                        if (lane == 0) trace_ev<TR>(j, t, 5);
+                        tc_fence_after();
+                    }
                     issue_pv(t, j, 1);
                     if (leader) {
                         if (!more) mma_commit(&o_final[t]);
@@ -835,6 +840,7 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     a.scale_log2 = x.scale * 1.4426950408889634f;
     a.heads = x.heads;
     a.batch = x.batch;
+    a.p_whole = tune_get("attn_pwhole", 0);
     static int sms = 0;
     if (!sms) {
         int dev = 0;

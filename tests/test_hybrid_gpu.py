@@ -9,7 +9,8 @@ the NCCL run uses ncclSend/Recv, and each group's ε̂ slot is broadcast from it
 where the NCCL run uses ncclBroadcast (engine.cpp hybrid_entry / step_exchange).
 
 Checked: every rank ends with the latent of a plain world=1 engine, bit for bit (a stage
-split moves the fp32 residual stream unchanged), and the activation bytes all ranks sent
+split moves the fp32 residual stream unchanged), and within the stated tolerance of the
+UNMODIFIED reference run_lp driving the fp32 oracle DiT; the activation bytes all ranks sent
 equal the reference's cost_hybrid intra-group bytes at hidden = d and 4-byte words.
 """
 import os
@@ -91,8 +92,11 @@ def _run(world, M, K, layers):
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,M,K,layers", [(2, 2, 1, 2), (4, 2, 2, 3), (3, 3, 1, 3)],
                          ids=["1group-2stages", "2groups-2stages-uneven", "1group-3stages"])
-def test_hybrid_groups_equal_plain_lp_and_cost_model(cuda, world, M, K, layers):
+def test_hybrid_groups_equal_plain_lp_and_cost_model(cuda, reference, world, M, K, layers):
+    import numpy as np
+
     from paper_2512_07350_b200 import lp
+    from tests.test_parity_schedule_gpu import _oracle
 
     res = _run(world, M, K, layers)
     outs = {out for _, out, _ in res}
@@ -105,6 +109,21 @@ def test_hybrid_groups_equal_plain_lp_and_cost_model(cuda, world, M, K, layers):
     want = ref.z.data.cpu().numpy().tobytes()
     ref.close()
     assert res[0][1] == want
+    # and against the oracle: the UNMODIFIED reference run_lp driving the fp32 oracle DiT (its own
+    # regenerated weights and text), at the stated per-step tolerance of
+    # tests/test_parity_schedule_gpu.py after the last step
+    torch.backends.cuda.matmul.allow_tf32 = False
+    refd, ck, cv, _ = _oracle(dit, cond)
+
+    def predict(zz, t, c, is_null):
+        return refd.predict(torch.from_numpy(zz).float().cuda(), t, ck, cv, 0 if is_null else 1).double().cpu().numpy()
+
+    os.environ["LPSIM_THREADS"] = "0"
+    final, _ = reference.run_lp_callback(predict, z, 4, STEPS, 0.05, 5.0, cond, PATCH, K, _r(K))
+    got = np.frombuffer(res[0][1], dtype=np.float32).reshape(DIMS).astype(np.float64)
+    rel = np.linalg.norm(got - final) / np.linalg.norm(final - np.asarray(z, np.float64))
+    assert np.isfinite(rel) and rel <= 1.5e-2, rel
+    assert np.abs(got - final).max() <= 5e-3 + 1e-3 * STEPS
     # stage layer ranges tile [0, L) and the activation traffic matches cost_hybrid
     spans = sorted((h["stage"], h["layer_begin"], h["layer_end"]) for _, _, h in res if h["group"] == 0)
     assert spans[0][1] == 0 and spans[-1][2] == layers

@@ -33,7 +33,13 @@ constexpr int kTile = 128;             // q rows per tile and kv rows per block
 constexpr int kHD = 128;               // head dim
 constexpr int kAtom = 128 * 128;       // one [128 rows x 128 B] swizzle block
 constexpr int kTileBytes = 2 * kAtom;  // [128 x 128] bf16 = 32 KB
-constexpr int kKStages = 3, kVStages = 2;
+#ifndef LP_ATTN_KS
+#define LP_ATTN_KS 3
+#endif
+#ifndef LP_ATTN_VS
+#define LP_ATTN_VS 2
+#endif
+constexpr int kKStages = LP_ATTN_KS, kVStages = LP_ATTN_VS;  // K / V ring depths (self-attention)
 constexpr int kAttnSmem = (2 /*Q0,Q1*/ + kKStages + kVStages) * kTileBytes + 1024 + 256;
 // NT = Q tiles per CTA.  NT = 2 (self-attention): the two tiles ping-pong inside the CTA,
 // K/V rings 3/2, 224 KB smem, all 512 TMEM columns, one CTA per SM.  NT = 1 (short key
@@ -210,7 +216,7 @@ __device__ __forceinline__ void softmax_block(uint32_t tS, uint32_t tO, int vali
             // CTA pair: one remote arrive per warp on the leader's barrier (count 8 = 4 warps x
             // 2 CTAs) once all 32 lanes' TMEM stores are complete
             __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(bar, 0);
+            if ((threadIdx.x & 31) == 0) mbar_arrive_remote(bar, 0);
         } else {
             mbar_arrive(bar);
         }

@@ -400,6 +400,22 @@ __device__ __forceinline__ void epi_chunk_smem(const GemmEpilogue& ep, int col0,
 #ifndef LP_EPI_RESID_DIST
 #define LP_EPI_RESID_DIST 2
 #endif
+// Accumulator-free handshake of the CTA-pair kernel: after its last TMEM read of a tile, each
+// epilogue warp (LP_TEMPTY_WARP=1, default) arrives once on the leader's tempty barrier with
+// the plain remote arrive; 0: every thread arrives with release.cluster semantics (a
+// cluster-scope fence per thread and tile — ncu: "membar" stalls).
+#ifndef LP_TEMPTY_WARP
+#define LP_TEMPTY_WARP 1
+#endif
+constexpr bool kTemptyWarp = LP_TEMPTY_WARP != 0;
+__device__ __forceinline__ void tempty_arrive(uint64_t* bar) {
+    if (kTemptyWarp) {
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive_remote(bar, 0);
+    } else {
+        mbar_arrive_cluster(bar, 0);
+    }
+}
 template <int MODE>
 constexpr int epi_boxes() { return kEpiTma ? (MODE == EPI_F32_RESID ? LP_EPI_RESID_BOXES : 2) : 0; }
 // XQ (LayerNorm-fold producer): two extra 2 KB bf16 boxes per epilogue warp for xq, paid for
@@ -451,7 +467,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 256);  // both CTAs' epilogue threads arrive on the leader's
+            // both CTAs' epilogue warps (LP_TEMPTY_WARP: one arrive per warp) or threads arrive
+            // on the leader's
+            mbar_init(&tempty[a], kTemptyWarp ? 8 : 256);
         }
         for (int b = 0; b < 16; ++b) mbar_init(&ebar[b], 1);
         fence_barrier_init();
@@ -602,7 +620,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             if (XQ && my_row < M)
                 ep.stats_out[static_cast<int64_t>(my_row) * num_n + nb] = ln_acc_final(ln.acc, static_cast<float>(BN));
             tc_fence_before();
-            mbar_arrive_cluster(&tempty[acc], 0);
+            tempty_arrive(&tempty[acc]);
         }
         if (lane == 0) bulk_wait_all();
         __syncwarp();
@@ -625,7 +643,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 if (row < M) epilogue_store<MODE>(ep, row, nb * BN + c, r);
             }
             tc_fence_before();
-            mbar_arrive_cluster(&tempty[acc], 0);
+            tempty_arrive(&tempty[acc]);
         }
     }
     tc_fence_before();

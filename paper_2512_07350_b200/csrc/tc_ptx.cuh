@@ -165,6 +165,17 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
         "r"(cta)
         : "memory");
 }
+// Same, with the default .release.cta semantics (the CUTLASS ClusterBarrier::arrive(cta) form):
+// no cluster-scope memory fence per arrive.  For handshakes whose data is tensor memory or
+// async-proxy traffic (ordered by tcgen05.fence / the mbarrier itself), not generic stores.
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+        "r"(cta)
+        : "memory");
+}
 // TMA load whose completion bytes are counted on the LEADER CTA's barrier (peer bit cleared)
 __device__ __forceinline__ void tma_load_2d_2sm(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1) {
     asm volatile(

@@ -74,6 +74,13 @@ struct AttnKernelArgs {
     int p_whole;  // MMA warp: wait for the whole P (p_full) before any PV instead of half by half
 };
 
+// p_half / p_full: one arrive per softmax warp instead of per thread (A/B build flag; measured
+// no gain in-step, 1120-1127 vs 1131-1132 TF/s, profiles/r3w)
+#ifndef LP_ATTN_WARP_ARRIVE
+#define LP_ATTN_WARP_ARRIVE 0
+#endif
+constexpr bool kWarpArrive = LP_ATTN_WARP_ARRIVE != 0;
+
 #ifndef LP_ATTN_MAX2
 constexpr bool kMax3 = true;
 #else
@@ -217,6 +224,11 @@ __device__ __forceinline__ void softmax_block(uint32_t tS, uint32_t tO, int vali
             // 2 CTAs) once all 32 lanes' TMEM stores are complete
             __syncwarp();
             if ((threadIdx.x & 31) == 0) mbar_arrive_remote(bar, 0);
+        } else if (kWarpArrive) {
+            // one arrive per warp (count 4): 128 per-thread arrivals serialise on one shared-
+            // memory word right on the softmax -> PV critical path
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
         } else {
             mbar_arrive(bar);
         }
@@ -306,8 +318,8 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
         }
         for (int s = 0; s < NT; ++s) {
             mbar_init(&s_full[s], 1);
-            mbar_init(&p_full[s], 128);
-            mbar_init(&p_half[s], 128);
+            mbar_init(&p_full[s], kWarpArrive ? 4 : 128);
+            mbar_init(&p_half[s], kWarpArrive ? 4 : 128);
             mbar_init(&o_final[s], 1);
             mbar_init(&o_empty[s], 128);
         }

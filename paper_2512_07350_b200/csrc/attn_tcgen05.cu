@@ -74,6 +74,24 @@ struct AttnKernelArgs {
     int p_whole;  // MMA warp: wait for the whole P (p_full) before any PV instead of half by half
 };
 
+// Waits of the TMA producer lane (K/V slot free) and of the softmax warps (S ready): spinning
+// try_wait (default) or try_wait with a suspend-time hint, so a waiting warp does not take
+// issue slots from the other tile's softmax warps on its SMSP (A/B build flags)
+#ifndef LP_ATTN_PROD_SLEEP
+#define LP_ATTN_PROD_SLEEP 0
+#endif
+#ifndef LP_ATTN_SM_SLEEP
+#define LP_ATTN_SM_SLEEP 0
+#endif
+__device__ __forceinline__ void pwait(uint64_t* bar, uint32_t parity) {
+    if (LP_ATTN_PROD_SLEEP) mbar_wait_sleep(bar, parity);
+    else mbar_wait(bar, parity);
+}
+__device__ __forceinline__ void swait(uint64_t* bar, uint32_t parity) {
+    if (LP_ATTN_SM_SLEEP) mbar_wait_sleep(bar, parity);
+    else mbar_wait(bar, parity);
+}
+
 // p_half / p_full: one arrive per softmax warp instead of per thread (A/B build flag; measured
 // no gain in-step, 1120-1127 vs 1131-1132 TF/s, profiles/r3w)
 #ifndef LP_ATTN_WARP_ARRIVE
@@ -354,7 +372,7 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
                 auto load_k = [&](int j) {
                     const uint32_t g = g0 + static_cast<uint32_t>(j);
                     const int s = static_cast<int>(g % KS);
-                    mbar_wait(&k_empty[s], ((g / KS) & 1u) ^ 1);
+                    pwait(&k_empty[s], ((g / KS) & 1u) ^ 1);
                     if (POLY == -2 && g >= KS) {  // debug (attn_trace=3): no TMA once the ring is primed
                         mbar_arrive(&k_full[s]);
                         return;
@@ -367,7 +385,7 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
                 auto load_v = [&](int j) {
                     const uint32_t g = g0 + static_cast<uint32_t>(j);
                     const int s = static_cast<int>(g % VS);
-                    mbar_wait(&v_empty[s], ((g / VS) & 1u) ^ 1);
+                    pwait(&v_empty[s], ((g / VS) & 1u) ^ 1);
                     if (POLY == -2 && g >= VS) {
                         mbar_arrive(&v_full[s]);
                         return;
@@ -489,7 +507,7 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
             const uint32_t g0 = PERS ? static_cast<uint32_t>(it) * static_cast<uint32_t>(nkv) : 0u;  // ring position base
             float m_run = -INFINITY, l_run = 0.f;
             for (int j = 0; j < nkv; ++j) {
-                mbar_wait(&s_full[t], ((g0 + static_cast<uint32_t>(j)) & 1u));
+                swait(&s_full[t], ((g0 + static_cast<uint32_t>(j)) & 1u));
                 const bool tr0 = TR && (warp & 3) == 2 && lane == 0;
                 if (tr0) trace_ev<TR>(j, t, 0);
                 tc_fence_after();

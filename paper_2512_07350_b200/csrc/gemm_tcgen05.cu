@@ -416,6 +416,16 @@ __device__ __forceinline__ void tempty_arrive(uint64_t* bar) {
         mbar_arrive_cluster(bar, 0);
     }
 }
+// CTA-pair kernel barrier waits: spinning try_wait (default) or try_wait with a suspend-time
+// hint, which parks the waiting warp instead of spending issue slots of the SMSP it shares
+// with an epilogue warp (A/B build flag LP_GEMM_WAIT_SLEEP)
+#ifndef LP_GEMM_WAIT_SLEEP
+#define LP_GEMM_WAIT_SLEEP 0
+#endif
+__device__ __forceinline__ void gwait(uint64_t* bar, uint32_t parity) {
+    if (LP_GEMM_WAIT_SLEEP) mbar_wait_sleep(bar, parity);
+    else mbar_wait(bar, parity);
+}
 template <int MODE>
 constexpr int epi_boxes() { return kEpiTma ? (MODE == EPI_F32_RESID ? LP_EPI_RESID_BOXES : 2) : 0; }
 // XQ (LayerNorm-fold producer): two extra 2 KB bf16 boxes per epilogue warp for xq, paid for
@@ -487,7 +497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             for (int t = cluster; t < tiles; t += nclusters) {
                 const int mb = t / num_n, nb = t % num_n;
                 for (int kb = 0; kb < nk; ++kb) {
-                    mbar_wait(&empty[s], ph ^ 1);
+                    gwait(&empty[s], ph ^ 1);
                     if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
                     tma_load_2d_2sm(&tma, &full[s], sA + s * A_BYTES, kb * kBK, mb * 2 * kBM + rank * kBM);
                     tma_load_2d_2sm(&tmb, &full[s], sB + s * B_BYTES, kb * kBK, nb * BN + rank * (BN / 2));
@@ -510,11 +520,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             for (int t = cluster; t < tiles; t += nclusters, ++it) {
                 const int acc = it & 1;
                 const uint32_t aph = (it >> 1) & 1;
-                mbar_wait(&tempty[acc], aph ^ 1);
+                gwait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + acc * BN;
                 for (int kb = 0; kb < nk; ++kb) {
-                    mbar_wait(&full[s], ph);
+                    gwait(&full[s], ph);
                     tc_fence_after();
                     if (leader) {
                         const uint64_t a0 = dA + static_cast<uint64_t>(s * A_BYTES >> 4);
@@ -567,7 +577,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             const int mb = t / num_n, nb = t % num_n;
             const int acc = it & 1;
             const uint32_t aph = (it >> 1) & 1;
-            mbar_wait(&tfull[acc], aph);
+            gwait(&tfull[acc], aph);
             tc_fence_after();
             const int row0 = mb * 2 * kBM + rank * kBM + q * 32;
             const uint32_t taddr = tmem + ((q * 32) << 16) + acc * BN;

@@ -431,26 +431,31 @@ constexpr int epi_boxes() { return kEpiTma ? (MODE == EPI_F32_RESID ? LP_EPI_RES
 // XQ (LayerNorm-fold producer): two extra 2 KB bf16 boxes per epilogue warp for xq, paid for
 // with one mainloop stage
 constexpr int kXqBox = 2048;
-template <int BN, int MODE = EPI_BF16, bool XQ = false>
+// KSUB: 64-wide K sub-blocks per pipeline stage.  KSUB = 2 halves the mainloop's barrier
+// checks and commits per FLOP (8 MMAs per full-barrier wait instead of 4: every check is a
+// tensor-pipe bubble, the issue being nearly synchronous) at the same bytes in flight
+// (half as many stages of twice the size).  Knob gemm_ksub; bf16-output epilogues only.
+template <int BN, int MODE = EPI_BF16, bool XQ = false, int KSUB = 1>
 constexpr int gemm2_stages() {
-    return (BN == 256 ? 6 : 8) - (epi_boxes<MODE>() > 2 ? (BN == 256 ? 1 : 2) : 0) - (XQ ? 1 : 0);
+    return ((BN == 256 ? 6 : 8) - (epi_boxes<MODE>() > 2 ? (BN == 256 ? 1 : 2) : 0) - (XQ ? 1 : 0)) / KSUB;
 }
-template <int BN, int MODE, bool XQ = false>
+template <int BN, int MODE, bool XQ = false, int KSUB = 1>
 constexpr int gemm2_smem_bytes() {
-    return gemm2_stages<BN, MODE, XQ>() * (kBM * kBK * 2 + (BN / 2) * kBK * 2) + 1024 + 512 +
+    return gemm2_stages<BN, MODE, XQ, KSUB>() * KSUB * (kBM * kBK * 2 + (BN / 2) * kBK * 2) + 1024 + 512 +
            4 * epi_boxes<MODE>() * kEpiBox + (XQ ? 4 * 2 * kXqBox : 0);
 }
 
-template <int BN, int MODE, bool XQ = false>
+template <int BN, int MODE, bool XQ = false, int KSUB = 1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
             const __grid_constant__ CUtensorMap tmo, const __grid_constant__ CUtensorMap tmq, GemmEpilogue ep, int M,
             int N, int K) {
-    constexpr int S = gemm2_stages<BN, MODE, XQ>();
+    constexpr int S = gemm2_stages<BN, MODE, XQ, KSUB>();
     constexpr int NB = epi_boxes<MODE>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    constexpr int A_BYTES = kBM * kBK * 2, B_BYTES = (BN / 2) * kBK * 2;
+    constexpr int A_SUB = kBM * kBK * 2, B_SUB = (BN / 2) * kBK * 2;
+    constexpr int A_BYTES = KSUB * A_SUB, B_BYTES = KSUB * B_SUB;
     uint8_t* sA = smem;
     uint8_t* sB = smem + S * A_BYTES;
     uint8_t* sE = sB + S * B_BYTES;  // [4 epilogue warps][NB][kEpiBox] (1024-aligned)
@@ -466,7 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const uint32_t rank = cluster_ctarank();
     const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
     const int num_n = N / BN, num_m = (M + 2 * kBM - 1) / (2 * kBM), tiles = num_m * num_n;
-    const int nk = (K + kBK - 1) / kBK;
+    const int nk = (K + KSUB * kBK - 1) / (KSUB * kBK);  // stages per tile (a ragged K tail is zero-filled)
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma);
@@ -499,8 +504,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 for (int kb = 0; kb < nk; ++kb) {
                     gwait(&empty[s], ph ^ 1);
                     if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
-                    tma_load_2d_2sm(&tma, &full[s], sA + s * A_BYTES, kb * kBK, mb * 2 * kBM + rank * kBM);
-                    tma_load_2d_2sm(&tmb, &full[s], sB + s * B_BYTES, kb * kBK, nb * BN + rank * (BN / 2));
+#pragma unroll
+                    for (int u = 0; u < KSUB; ++u) {
+                        const int kc = (kb * KSUB + u) * kBK;
+                        tma_load_2d_2sm(&tma, &full[s], sA + s * A_BYTES + u * A_SUB, kc, mb * 2 * kBM + rank * kBM);
+                        tma_load_2d_2sm(&tmb, &full[s], sB + s * B_BYTES + u * B_SUB, kc, nb * BN + rank * (BN / 2));
+                    }
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
@@ -530,8 +539,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                         const uint64_t a0 = dA + static_cast<uint64_t>(s * A_BYTES >> 4);
                         const uint64_t b0 = dB + static_cast<uint64_t>(s * B_BYTES >> 4);
 #pragma unroll
-                        for (int k = 0; k < kBK / 16; ++k)
-                            mma_ss_2sm(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);  // +32 B per K=16
+                        for (int u = 0; u < KSUB; ++u)
+#pragma unroll
+                            for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 inside a sub-block
+                                mma_ss_2sm(d, a0 + (u * A_SUB >> 4) + 2 * k, b0 + (u * B_SUB >> 4) + 2 * k, idesc,
+                                           (kb | u | k) != 0);
                         mma_commit_2sm(&empty[s], 0x3);
                     }
                     __syncwarp();
@@ -689,18 +701,24 @@ static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Gemm
     LP_LAUNCH_CHECK();
 }
 
-template <int BN, int MODE, bool XQ>
+template <int BN, int MODE, bool XQ, int KSUB = 1>
 static void launch_gemm2_x(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& tq,
                            const GemmEpilogue& ep, int M, int N, int K, cudaStream_t st) {
-    constexpr int smem = gemm2_smem_bytes<BN, MODE, XQ>();
+    if constexpr (KSUB == 1 && BN == 256 && !XQ && (MODE == EPI_BF16 || MODE == EPI_BF16_GELU)) {
+        if (tune_get("gemm_ksub", 1) == 2 && K % (2 * kBK) == 0) {
+            launch_gemm2_x<BN, MODE, XQ, 2>(ta, tb, to, tq, ep, M, N, K, st);
+            return;
+        }
+    }
+    constexpr int smem = gemm2_smem_bytes<BN, MODE, XQ, KSUB>();
     static bool attr = false;
     if (!attr) {
-        LP_CUDA(cudaFuncSetAttribute(k_gemm2<BN, MODE, XQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        LP_CUDA(cudaFuncSetAttribute(k_gemm2<BN, MODE, XQ, KSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
     }
     const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * (N / BN);
     const int clusters = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-    k_gemm2<BN, MODE, XQ><<<2 * clusters, kGemmThreads, smem, st>>>(ta, tb, to, tq, ep, M, N, K);
+    k_gemm2<BN, MODE, XQ, KSUB><<<2 * clusters, kGemmThreads, smem, st>>>(ta, tb, to, tq, ep, M, N, K);
     LP_LAUNCH_CHECK();
 }
 

@@ -70,6 +70,32 @@ def _attn(q, k, v, scale):
     return o
 
 
+@pytest.mark.parametrize("mode", [0, 1], ids=["bf16", "bf16-gelu"])
+@pytest.mark.parametrize("M,N,K", [(300, 1536, 1536), (1000, 8960, 512), (4097, 4608, 1536), (257, 256, 128)])
+def test_gemm_two_subblock_stages_match_torch(cuda, mode, M, N, K):
+    """CTA-pair GEMM with two 64-wide K sub-blocks per pipeline stage (knob gemm_ksub=2: 8 MMAs
+    per full-barrier wait) vs torch fp32, and bit-identical to the one-sub-block pipeline (same
+    MMAs in the same order)."""
+    g = torch.Generator(device="cuda").manual_seed(M + 5 * N + K + mode)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g)
+    outs = []
+    for ks in (1, 2):
+        _lib.check(_lib.lib().lp_tune(b"gemm_ksub", ks))
+        D = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        _lib.check(_lib.lib().lp_gemm_bf16_epi(C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()),
+                                               C.c_void_p(bias.data_ptr()), C.c_void_p(bias.data_ptr()),
+                                               C.c_void_p(D.data_ptr()), M, N, K, mode,
+                                               C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        outs.append(D)
+    _lib.check(_lib.lib().lp_tune(b"gemm_ksub", 1))
+    y = A.float() @ B.float().t() + bias
+    ref = y if mode == 0 else torch.nn.functional.gelu(y, approximate="tanh")
+    assert (outs[1].float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-2
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("B,S,Skv,H", [(1, 128, 128, 1), (2, 200, 200, 3), (2, 300, 512, 2), (1, 1024, 1024, 2),
                                        (2, 1560, 1560, 12), (1, 129, 1000, 1)])
 def test_attention_matches_torch(cuda, B, S, Skv, H):

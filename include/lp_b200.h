@@ -453,8 +453,10 @@ int lp_engine_exchange_bench(lp_engine* e, int32_t step, int32_t iters, void* st
 /* K1 and K10 alone, for their HBM roofline: `iters` back-to-back launches each of step's K1
  * (gather of this rank's windows) and K10 (blend + sampler update of the full latent), on
  * `sets` private copies of (z, shards, gathered ε̂) used round robin so consecutive launches
- * stream from HBM, not L2.  out = {K1 ms per launch, K1 algorithmic bytes per launch, K10 ms
- * per launch, K10 algorithmic bytes per launch}; the engine's own z is untouched. */
+ * stream from HBM, not L2.  Each loop of `iters` launches is captured once and replayed as a
+ * CUDA graph, timed with events on `stream` (no host launch gaps between the few-µs kernels).
+ * out = {K1 ms per launch, K1 algorithmic bytes per launch, K10 ms per launch, K10 algorithmic
+ * bytes per launch}; the engine's own z is untouched. */
 int lp_engine_hbm_bench(lp_engine* e, int32_t step, int32_t iters, int32_t sets, void* stream, double out[4]);
 /* Bytes this engine moved over NCCL so far, and the reference ledger bytes. */
 int lp_engine_comm(const lp_engine* e, uint64_t* nccl_bytes, uint64_t* ledger_bytes);

@@ -77,6 +77,9 @@ struct AttnKernelArgs {
 // Waits of the TMA producer lane (K/V slot free) and of the softmax warps (S ready): spinning
 // try_wait (default) or try_wait with a suspend-time hint, so a waiting warp does not take
 // issue slots from the other tile's softmax warps on its SMSP (A/B build flags)
+#ifndef LP_ATTN_MMA_SPIN
+#define LP_ATTN_MMA_SPIN 0
+#endif
 #ifndef LP_ATTN_PROD_SLEEP
 #define LP_ATTN_PROD_SLEEP 0
 #endif
@@ -417,7 +420,10 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
         // warp-wide waits that suspend in hardware (try_wait with a time hint) instead of
         // spinning: 32 spinning lanes would steal issue slots from the softmax warps sharing
         // this SMSP
-        auto wait1 = [&](uint64_t* bar, uint32_t parity) { mbar_wait_sleep(bar, parity); };
+        auto wait1 = [&](uint64_t* bar, uint32_t parity) {
+            if (LP_ATTN_MMA_SPIN) mbar_wait(bar, parity);  // A/B build flag: spinning try_wait
+            else mbar_wait_sleep(bar, parity);
+        };
         constexpr uint32_t idS = idesc_bf16(128, 128);
         constexpr uint32_t idO = idesc_bf16(128, 128, /*b_mn_major=*/true);
         // descriptors built once; per-k offsets go into the start-address field (addr >> 4)

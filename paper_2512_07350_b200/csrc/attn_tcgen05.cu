@@ -618,7 +618,13 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
 // o_final), and both CTAs' softmax warps arrive on the leader's p_half / p_full (count 8).
 // The softmax and epilogue are the single-CTA kernel's.
 // ---------------------------------------------------------------------------
-constexpr int kPairKS = 4, kPairVS = 4;
+#ifndef LP_PAIR_KS
+#define LP_PAIR_KS 4
+#endif
+#ifndef LP_PAIR_VS
+#define LP_PAIR_VS 4
+#endif
+constexpr int kPairKS = LP_PAIR_KS, kPairVS = LP_PAIR_VS;  // K / V ring depths of the pair kernel
 constexpr int kHalfTile = 64 * 128 * 2;  // 16 KB: [64 keys x 128 dims] (K) or [128 keys x 64 dims] (V)
 constexpr int kPairSmem = 2 * kTileBytes + (kPairKS + kPairVS) * kHalfTile + 1024 + 256;
 

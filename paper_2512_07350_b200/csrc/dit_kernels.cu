@@ -163,13 +163,20 @@ void time_embedding(const TimeWeights& w, const float* t_dev, int freq_dim, int 
 //   MOD:    y = LN(x) * (1 + scale) + shift
 //   AFFINE: y = LN(x) * weight + bias
 // ---------------------------------------------------------------------------
+// Row order of the row-wise HBM passes (LayerNorm, q/k RMSNorm+RoPE; knob row_rev): the GEMM
+// that wrote their input finished on its last rows, which are the ones still in L2, and the
+// GEMM that reads their output starts on its first rows — so walking rows last-to-first lets
+// both ends of each pass meet L2 instead of HBM.  Results are identical (rows independent).
+static int row_order_rev() { return tune_get("row_rev", 0); }
+
 template <int PER, bool AFFINE>
 __global__ void __launch_bounds__(256) k_layernorm(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
                                                    int64_t rows, int d, const float* __restrict__ a,
-                                                   const float* __restrict__ b, float eps) {
-    const int64_t row = blockIdx.x * 8LL + threadIdx.x / 32;
+                                                   const float* __restrict__ b, float eps, int rev) {
+    int64_t row = blockIdx.x * 8LL + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
+    if (rev) row = rows - 1 - row;  // last-written rows first (see row_order_rev)
     const float4* xr = reinterpret_cast<const float4*>(x + row * d);
     float v[PER * 4];
     float s = 0.f;
@@ -214,11 +221,12 @@ void layernorm_bf16(const float* x, __nv_bfloat16* y, int64_t rows, int d, const
                     float eps, cudaStream_t st) {
     if (d % 128) fail(LP_ERR_INVALID_ARGUMENT, "layernorm: d must be a multiple of 128");
     const int per = d / 128;
+    const int rev = row_order_rev();
     const unsigned g = static_cast<unsigned>((rows + 7) / 8);
 #define LP_LN(P)                                                                                 \
     if (per == P) {                                                                              \
-        if (affine) k_layernorm<P, true><<<g, 256, 0, st>>>(x, y, rows, d, a, b, eps);           \
-        else k_layernorm<P, false><<<g, 256, 0, st>>>(x, y, rows, d, a, b, eps);                 \
+        if (affine) k_layernorm<P, true><<<g, 256, 0, st>>>(x, y, rows, d, a, b, eps, rev);      \
+        else k_layernorm<P, false><<<g, 256, 0, st>>>(x, y, rows, d, a, b, eps, rev);            \
         LP_LAUNCH_CHECK();                                                                       \
         return;                                                                                  \
     }
@@ -446,7 +454,7 @@ __global__ void __launch_bounds__(256, LP_RMS_MINB) k_rmsnorm_rope_tab(__nv_bflo
                                                           int64_t col0, int nsec, const float* __restrict__ g0,
                                                           const float* __restrict__ g1, float eps,
                                                           const float2* __restrict__ tab, const RopeDivs dv,
-                                                          int nf, int nh, int nw) {
+                                                          int nf, int nh, int nw, int rev) {
     constexpr int d = PER8 * 256;
     // 32-bit index math with multiply-shift division (the host checks the ranges): the
     // former 64-bit div/mod sequences cost more issue slots than the row's arithmetic.
@@ -456,6 +464,7 @@ __global__ void __launch_bounds__(256, LP_RMS_MINB) k_rmsnorm_rope_tab(__nv_bflo
     const int lane = threadIdx.x & 31;
     uint32_t wid = blockIdx.x * 8u + threadIdx.x / 32;
     auto unit_ptr = [&](uint32_t w) {
+        if (rev) w = units - 1u - w;
         const uint32_t row = nsec == 2 ? w >> 1 : w;
         const int sec = nsec == 2 ? static_cast<int>(w & 1u) : 0;
         return reinterpret_cast<uint4*>(buf + static_cast<int64_t>(row) * ld + col0 + static_cast<int64_t>(sec) * d);
@@ -467,8 +476,9 @@ __global__ void __launch_bounds__(256, LP_RMS_MINB) k_rmsnorm_rope_tab(__nv_bflo
         for (int i = 0; i < PER8; ++i) nxt[i] = p0[lane + 32 * i];
     }
     for (; wid < units; wid += nwarps) {
-        const uint32_t row = nsec == 2 ? wid >> 1 : wid;
-        const int sec = nsec == 2 ? static_cast<int>(wid & 1u) : 0;
+        const uint32_t u = rev ? units - 1u - wid : wid;
+        const uint32_t row = nsec == 2 ? u >> 1 : u;
+        const int sec = nsec == 2 ? static_cast<int>(u & 1u) : 0;
         uint4* p = unit_ptr(wid);
         const float* g = sec ? g1 : g0;
 #pragma unroll
@@ -506,9 +516,10 @@ bool rmsnorm_rope_tab(__nv_bfloat16* buf, int64_t rows, int64_t ld, int64_t col0
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const unsigned gr = static_cast<unsigned>(std::min<int64_t>((rows * nsec + 7) / 8, static_cast<int64_t>(sms) * LP_RMS_MINB));
+    const int rev = row_order_rev();
 #define LP_RMT(P)                                                                                                   \
     if (d == 256 * P) {                                                                                             \
-        k_rmsnorm_rope_tab<P><<<gr, 256, 0, st>>>(buf, rows, ld, col0, nsec, g0, g1, eps, tab, dv, nf, nh, nw);    \
+        k_rmsnorm_rope_tab<P><<<gr, 256, 0, st>>>(buf, rows, ld, col0, nsec, g0, g1, eps, tab, dv, nf, nh, nw, rev); \
         LP_LAUNCH_CHECK();                                                                                          \
         return true;                                                                                                \
     }

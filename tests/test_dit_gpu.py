@@ -273,6 +273,19 @@ def test_block0_self_attention_dedupe_is_bit_identical(cuda):
     assert torch.equal(outs[0], outs[1])
 
 
+def test_row_order_reversal_is_bit_identical(cuda):
+    """LayerNorm and q/k RMSNorm+RoPE passes walking rows last-to-first (knob row_rev, for L2
+    reuse with the neighbouring GEMMs) give the same bits as the forward order."""
+    z, cond = lp.synthetic_latent((16, 5, 16, 16), 4, 2025)
+    dit = lp.DiTDenoiser(cond, num_layers=2)
+    outs = []
+    for on in (0, 1):
+        _lib.check(_lib.lib().lp_tune(b"row_rev", on))
+        outs.append(dit.cfg_predict(z, 9, 5.0).data.clone())
+    _lib.check(_lib.lib().lp_tune(b"row_rev", 0))
+    assert torch.equal(outs[0], outs[1])
+
+
 def test_text_context_kv_all_layers_vs_oracle(cuda):
     """The cached cross-attention K/V of all 30 layers, uncond (null text) and cond (synthetic
     text) halves, vs the oracle's fp32 restatement: its own text generator, text MLP, K/V

@@ -72,6 +72,8 @@ struct AttnKernelArgs {
     float scale_log2;  // softmax scale * log2(e)
     int heads, batch;
     int p_whole;  // MMA warp: wait for the whole P (p_full) before any PV instead of half by half
+    const void* q;        // raw Q (the TMEM-resident-Q instance loads its rows directly)
+    int64_t ldq, q_total_rows;
 };
 
 // Waits of the TMA producer lane (K/V slot free) and of the softmax warps (S ready): spinning
@@ -840,6 +842,336 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAttnThreads, 1)
     if (warp == 2) tmem_dealloc_2sm(tmem, 512);
 }
 
+// ---------------------------------------------------------------------------
+// Self-attention, CTA pair with Q resident in TMEM and S double-buffered (knob attn_qtm).
+// Each CTA of a 2-CTA cluster owns ONE 128-row Q tile (256 query rows per pair).  Q is loaded
+// once into TMEM (in the A-operand layout P uses), so S = Q K^T is a TS MMA (M = 256, the pair)
+// that reads only K from shared memory; two S buffers let S(j+1) run while the softmax of
+// block j does.  Per SM and 128-key block: S reads 32 KB, PV 32 KB, TMA writes 32 KB (96 KB vs
+// 256 KB for the two-tile kernel: its SS S-MMAs alone use the whole ~128 B/clk operand path,
+// profiles/r4h), and the softmax -> PV -> S chain is off the critical path.
+// TMEM per CTA: Q [0,64) | S0 [128,256) | S1 [256,384) | O [384,512).
+// A rare O rescale waits for the previous PV (o_done[(j-1) & 1]): the next PV that can
+// complete needs this block's P, so those barriers never run a full phase ahead.
+// ---------------------------------------------------------------------------
+constexpr int kQtKS = 6, kQtVS = 6;
+constexpr int kQtThreads = 64 + 256;  // TMA, MMA, two softmax warpgroups
+constexpr int kQtSmem = (kQtKS + kQtVS) * kHalfTile + 1024 + 512 + 4096 + 1024;
+
+// One 128-key block for one query row, split over TWO softmax warpgroups: warpgroup h owns key
+// columns [64h, 64h + 64) of the row.  The row max is exchanged through shared memory (xch,
+// double-buffered by block parity; a 64-thread named barrier per TMEM lane quarter), so both
+// halves keep the same running max and rescale decision; each half keeps its own partial row
+// sum, rescales its 64 columns of O, and writes its P as packed bf16 over the first 32 columns of
+// ITS OWN S half (already read: keys [64h, 64h+64) -> S columns [64h, 64h+32)), published on
+// p_half (h = 0) or p_full (h = 1): PV's first four k-steps read P at +0, the last four at +64.
+template <int POLY, bool MASK>
+__device__ __forceinline__ void softmax_half_qt(uint32_t tS, uint32_t tO, int valid, float c, float& m_run,
+                                                float& l_run, uint64_t* p_bar, uint64_t* o_bar, uint32_t o_par,
+                                                bool have_prev, int h, float* xch, int row, uint32_t qbar) {
+    const int k0 = 64 * h;  // this half's first key column
+    float mx;
+    {
+        uint32_t r[64];
+        tmem_ld32(tS + k0, *reinterpret_cast<uint32_t(*)[32]>(r));
+        tmem_ld32(tS + k0 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+        tmem_ld_wait();
+        if (MASK) {
+#pragma unroll
+            for (int u = 0; u < 64; ++u)
+                if (k0 + u >= valid) r[u] = __float_as_uint(-INFINITY);
+        }
+        float m8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) m8[u] = fmaxf(__uint_as_float(r[u]), __uint_as_float(r[u + 8]));
+#pragma unroll
+        for (int u = 16; u < 64; u += 16)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) m8[k] = fmax3(m8[k], __uint_as_float(r[u + k]), __uint_as_float(r[u + 8 + k]));
+        mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+    }
+    xch[h * 128 + row] = mx;
+    named_bar_sync(qbar, 64);
+    mx = fmaxf(mx, xch[(h ^ 1) * 128 + row]);
+    const bool need = m_run == -INFINITY || (mx - m_run) * c > 8.f;
+    if (__any_sync(0xffffffff, need && m_run != -INFINITY)) {
+        if (have_prev) mbar_wait(o_bar, o_par);  // O holds PV(j-1) before it is rescaled
+        tc_fence_after();
+        const float alpha = need && m_run != -INFINITY ? ex2((m_run - mx) * c) : 1.f;
+#pragma unroll 1
+        for (int cc = 0; cc < 64; cc += 32) {
+            uint32_t r[32];
+            tmem_ld32(tO + k0 + cc, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int u = 0; u < 32; ++u) r[u] = __float_as_uint(__uint_as_float(r[u]) * alpha);
+            tmem_st32(tO + k0 + cc, r);
+        }
+        l_run *= alpha;
+    }
+    if (need) m_run = mx;
+    const float2 c2 = make_float2(c, c), nmc2 = make_float2(-m_run * c, -m_run * c);
+    float2 lsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    auto chunk = [&](const uint32_t (&r)[32], int cc) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            float2 sx = make_float2(__uint_as_float(r[2 * u]), __uint_as_float(r[2 * u + 1]));
+            if (MASK) {
+                if (k0 + cc + 2 * u >= valid) sx.x = -INFINITY;
+                if (k0 + cc + 2 * u + 1 >= valid) sx.y = -INFINITY;
+            }
+            const float2 x = __ffma2_rn(sx, c2, nmc2);
+            float2 pv;
+            if (POLY > 0 && ((u * 5) & 15) < POLY) {
+                pv = ex2_poly2(x);
+            } else {
+                pv.x = ex2(x.x);
+                pv.y = ex2(x.y);
+            }
+            lsum[u & 1] = __fadd2_rn(lsum[u & 1], pv);
+            pk[u] = pack_bf16(pv.x, pv.y);
+        }
+        tmem_st16(tS + k0 + cc / 2, pk);
+    };
+    uint32_t ra[32], rb[32];
+    tmem_ld32(tS + k0, ra);
+    tmem_ld_wait();
+    tmem_ld32(tS + k0 + 32, rb);
+    chunk(ra, 0);
+    tmem_ld_wait();
+    chunk(rb, 32);
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive_remote(p_bar, 0);
+    const float2 ls = __fadd2_rn(lsum[0], lsum[1]);
+    l_run += ls.x + ls.y;
+}
+
+template <int POLY>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kQtThreads, 1)
+    k_attention_qt(const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
+                   const __grid_constant__ CUtensorMap to, AttnKernelArgs a) {
+    constexpr int KS = kQtKS, VS = kQtVS;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = smem;                    // [KS][2 atoms of 64 rows x 128 B]  (this CTA's 64 keys)
+    uint8_t* sV = sK + KS * kHalfTile;     // [VS][1 atom of 128 rows x 128 B]  (this CTA's 64 dims)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VS * kHalfTile);
+    uint64_t* q_ready = bars + 0;          // leader: both CTAs' Q rows in TMEM (8 warps)
+    uint64_t* k_full = q_ready + 1;        // leader [KS]
+    uint64_t* k_empty = k_full + KS;       // [KS]
+    uint64_t* v_full = k_empty + KS;       // leader [VS]
+    uint64_t* v_empty = v_full + VS;       // [VS]
+    uint64_t* s_full = v_empty + VS;       // [2] S(j) in buffer j & 1
+    uint64_t* p_half = s_full + 2;         // leader [2]
+    uint64_t* p_full = p_half + 2;         // leader [2]
+    uint64_t* o_done = p_full + 2;         // [2] PV(j) complete, j & 1
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+    float* xch = reinterpret_cast<float*>(bars + 64);   // [2 block parity][2 halves][128 rows] row maxima
+    float* lxch = xch + 2 * 2 * 128;                   // [2 halves][128 rows] partial row sums
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const uint32_t rank = cluster_ctarank();
+    const int nkv = static_cast<int>((a.n_kv + kTile - 1) / kTile);
+    const int qt = static_cast<int>(blockIdx.x), h = static_cast<int>(blockIdx.y), b = static_cast<int>(blockIdx.z);
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tk);
+        tma_prefetch(&tv);
+        mbar_init(q_ready, 16);  // 8 softmax warps x 2 CTAs
+        for (int s = 0; s < KS; ++s) {
+            mbar_init(&k_full[s], 1);
+            mbar_init(&k_empty[s], 1);
+        }
+        for (int s = 0; s < VS; ++s) {
+            mbar_init(&v_full[s], 1);
+            mbar_init(&v_empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_half[i], 8);  // warpgroup 0's 4 warps x 2 CTAs (keys 0..63)
+            mbar_init(&p_full[i], 8);  // warpgroup 1's (keys 64..127)
+            mbar_init(&o_done[i], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_2sm(tmem_slot, 512);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    constexpr uint32_t kColQ = 0, kColS = 128, kColO = 384;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const int32_t kc = static_cast<int32_t>(a.k_col0 + h * kHD);
+            const int32_t vc = static_cast<int32_t>(a.v_col0 + h * kHD + rank * 64);
+            auto load_k = [&](int j) {
+                const int s = j % KS;
+                mbar_wait(&k_empty[s], ((j / KS) & 1) ^ 1);
+                if (rank == 0) mbar_arrive_expect_tx(&k_full[s], 2 * kHalfTile);
+                const int32_t kr = static_cast<int32_t>(b * a.kv_rows_per_batch + j * kTile + rank * 64);
+                tma_load_2d_2sm(&tk, &k_full[s], sK + s * kHalfTile, kc, kr);
+                tma_load_2d_2sm(&tk, &k_full[s], sK + s * kHalfTile + kHalfTile / 2, kc + 64, kr);
+            };
+            auto load_v = [&](int j) {
+                const int s = j % VS;
+                mbar_wait(&v_empty[s], ((j / VS) & 1) ^ 1);
+                if (rank == 0) mbar_arrive_expect_tx(&v_full[s], 2 * kHalfTile);
+                const int32_t kr = static_cast<int32_t>(b * a.kv_rows_per_batch + j * kTile);
+                tma_load_2d_2sm(&tv, &v_full[s], sV + s * kHalfTile, vc, kr);
+            };
+            int jk = 0;
+            for (; jk < nkv && jk < KS - 1; ++jk) load_k(jk);
+            for (int j = 0; j < nkv; ++j) {
+                load_v(j);
+                if (jk < nkv) load_k(jk++);
+            }
+        }
+    } else if (warp == 1) {
+        if (rank == 0) {
+            const bool leader = elect_one();
+            constexpr uint32_t idS = idesc_bf16(256, 128);                      // A (Q) from TMEM, B = K K-major
+            constexpr uint32_t idO = idesc_bf16(256, 128, /*b_mn_major=*/true);  // A (P) from TMEM, B = V MN-major
+            const uint64_t dK = desc_sw128(smem_u32(sK));
+            const uint64_t dV = desc_sw128(smem_u32(sV), /*sbo=*/1024, /*lbo=*/kAtom);
+            mbar_wait_sleep(q_ready, 0);
+            tc_fence_after();
+            auto issue_s = [&](int j) {
+                const int s = j % KS;
+                mbar_wait_sleep(&k_full[s], (j / KS) & 1);
+                tc_fence_after();
+                if (leader) {
+                    const uint64_t k0 = dK + s * (kHalfTile >> 4);
+                    const uint32_t dS = tmem + kColS + (j & 1) * 128;
+#pragma unroll
+                    for (int k = 0; k < kHD / 16; ++k) {
+                        const uint64_t ok = static_cast<uint64_t>((k >> 2) * (kHalfTile / 2) + (k & 3) * 32) >> 4;
+                        mma_ts_2sm(dS, tmem + kColQ + k * 8, k0 + ok, idS, k != 0);
+                    }
+                    mma_commit_2sm(&s_full[j & 1], 0x3);
+                    mma_commit_2sm(&k_empty[s], 0x3);
+                }
+                __syncwarp();
+            };
+            issue_s(0);
+            if (nkv > 1) issue_s(1);
+            for (int j = 0; j < nkv; ++j) {
+                const int bb = j & 1;
+                const uint32_t par = (j >> 1) & 1;
+                const uint32_t tP = tmem + kColS + bb * 128;
+                const uint64_t v0 = dV + (j % VS) * (kHalfTile >> 4);
+                mbar_wait_sleep(&p_half[bb], par);
+                mbar_wait_sleep(&v_full[j % VS], (j / VS) & 1);
+                tc_fence_after();
+                if (leader) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        mma_ts_2sm(tmem + kColO, tP + k * 8, v0 + ((k * 2048) >> 4), idO, (j | k) != 0);
+                }
+                __syncwarp();
+                mbar_wait_sleep(&p_full[bb], par);
+                tc_fence_after();
+                if (leader) {
+#pragma unroll
+                    for (int k = 4; k < 8; ++k)  // keys 64..127: P at +64 (the second half's own S columns)
+                        mma_ts_2sm(tmem + kColO, tP + 64 + (k - 4) * 8, v0 + ((k * 2048) >> 4), idO, true);
+                    mma_commit_2sm(&o_done[bb], 0x3);
+                    mma_commit_2sm(&v_empty[j % VS], 0x3);
+                }
+                __syncwarp();
+                if (j + 2 < nkv) issue_s(j + 2);  // into buffer bb, after PV(j) read its P (in order)
+            }
+        }
+    } else {
+        // two softmax warpgroups (warps 2..5: keys 0..63, 6..9: keys 64..127 of every block);
+        // thread <-> query row / TMEM lane, the two warps of a lane quarter meet on named barrier 1+q
+        const int hh = (static_cast<int>(warp) - 2) >> 2;
+        const uint32_t q = warp & 3;
+        const int row = q * 32 + lane;
+        const uint32_t lane_off = (q * 32) << 16;
+        const uint32_t qbar = 1 + q;
+        // this half's 64 dims of the Q row -> TMEM columns [32 hh, 32 hh + 32) (packed bf16 pairs,
+        // the A-operand layout of P)
+        {
+            const int64_t grow = static_cast<int64_t>(b) * a.q_rows_per_batch + static_cast<int64_t>(qt) * kTile + row;
+            uint32_t w[32];
+            if (grow < a.q_total_rows) {
+                const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.q) + grow * a.ldq +
+                                                                  a.q_col0 + h * kHD + 64 * hh);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(w + 4 * i) = src[i];
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) w[i] = 0u;
+            }
+            tmem_st32(tmem + lane_off + kColQ + 32 * hh, w);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(q_ready, 0);
+        }
+        const uint32_t tO = tmem + lane_off + kColO;
+        const float c = a.scale_log2;
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int j = 0; j < nkv; ++j) {
+            const int bb = j & 1;
+            swait(&s_full[bb], (j >> 1) & 1);
+            tc_fence_after();
+            const uint32_t tS = tmem + lane_off + kColS + bb * 128;
+            const int valid = static_cast<int>(a.n_kv - static_cast<int64_t>(j) * kTile);
+            uint64_t* ob = &o_done[(j - 1) & 1];
+            const uint32_t opar = static_cast<uint32_t>(((j - 1) >> 1) & 1);
+            uint64_t* pb = hh == 0 ? &p_half[bb] : &p_full[bb];
+            float* xj = xch + bb * 256;
+            if (valid >= kTile)
+                softmax_half_qt<POLY, false>(tS, tO, valid, c, m_run, l_run, pb, ob, opar, j > 0, hh, xj, row, qbar);
+            else
+                softmax_half_qt<POLY, true>(tS, tO, valid, c, m_run, l_run, pb, ob, opar, j > 0, hh, xj, row, qbar);
+        }
+        // epilogue: the row sum over both halves, the last PV, then this half's 64 columns of
+        // O / l -> bf16 staged as atom hh in K ring slots 0..1 (every S MMA, the last readers of
+        // K, completed before the last PV), one TMA store per warp
+        lxch[hh * 128 + row] = l_run;
+        named_bar_sync(qbar, 64);
+        l_run = l_run + lxch[(hh ^ 1) * 128 + row];  // commutative: the same total in both halves
+        mbar_wait(&o_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
+        tc_fence_after();
+        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+        uint8_t* stage = sK;
+#pragma unroll 1
+        for (int cc = 0; cc < 64; cc += 32) {
+            uint32_t r[32];
+            tmem_ld32(tO + 64 * hh + cc, r);
+            tmem_ld_wait();
+            uint8_t* arow = stage + hh * kAtom + row * 128;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int unit = (cc >> 3) + u;
+                *reinterpret_cast<uint4*>(arow + ((unit ^ (row & 7)) << 4)) =
+                    make_uint4(pack_bf16(__uint_as_float(r[8 * u + 0]) * inv, __uint_as_float(r[8 * u + 1]) * inv),
+                               pack_bf16(__uint_as_float(r[8 * u + 2]) * inv, __uint_as_float(r[8 * u + 3]) * inv),
+                               pack_bf16(__uint_as_float(r[8 * u + 4]) * inv, __uint_as_float(r[8 * u + 5]) * inv),
+                               pack_bf16(__uint_as_float(r[8 * u + 6]) * inv, __uint_as_float(r[8 * u + 7]) * inv));
+            }
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+            const int32_t r0 = static_cast<int32_t>(qt * kTile + q * 32);
+            tma_store_3d(&to, stage + hh * kAtom + q * 32 * 128, static_cast<int32_t>(h * kHD + hh * 64), r0, b);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        __syncwarp();
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) tmem_dealloc_2sm(tmem, 512);
+}
+
 static int attn_poly() {
     // pairs out of every 16 whose exp2 runs on the FMA pipe (0, 4, 6 compiled; A/B r1n: 6 best)
     const int v = tune_get("attn_poly", 6);
@@ -866,6 +1198,7 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
         LP_CUDA(cudaFuncSetAttribute(k_attention<6, false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kAttnSmem));
         LP_CUDA(cudaFuncSetAttribute(k_attention_pair<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
+        LP_CUDA(cudaFuncSetAttribute(k_attention_qt<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, kQtSmem));
         attr = true;
     }
     if ((x.ldq | x.ldk | x.ldv | x.ldo) % 8) fail(LP_ERR_INVALID_ARGUMENT, "attention: strides must be multiples of 8");
@@ -889,6 +1222,9 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     a.heads = x.heads;
     a.batch = x.batch;
     a.p_whole = tune_get("attn_pwhole", 0);
+    a.q = x.q;
+    a.ldq = x.ldq;
+    a.q_total_rows = x.q_total_rows;
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -915,6 +1251,12 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     } else if (nt1) {
         const dim3 g1(static_cast<unsigned>((x.n_q + kTile - 1) / kTile), x.heads, x.batch);
         k_attention<6, false, 1><<<g1, AttnCfg<1>::threads, AttnCfg<1>::smem, st>>>(tq, tk, tv, to, a);
+    } else if (ok_p && tune_get("attn_qtm", 0) && x.ldq % 8 == 0 && (x.q_col0 % 8) == 0) {
+        // CTA pairs, one Q tile per CTA resident in TMEM, double-buffered S (self-attention)
+        const CUtensorMap tk64 = make_tmap_2d_bf16(x.k, x.ldk, x.kv_total_rows, x.ldk * 2, 64, 64);
+        const unsigned tiles = static_cast<unsigned>((x.n_q + kTile - 1) / kTile);
+        const dim3 gq((tiles + 1) / 2 * 2, x.heads, x.batch);
+        k_attention_qt<6><<<gq, kQtThreads, kQtSmem, st>>>(tk64, tv, to, a);
     } else if (ok_p && tune_get("attn_pair", 0)) {
         // CTA pairs (self-attention): the K map's box is 64 key rows (each CTA loads half a block)
         const CUtensorMap tk64 = make_tmap_2d_bf16(x.k, x.ldk, x.kv_total_rows, x.ldk * 2, 64, 64);

@@ -111,10 +111,12 @@ def test_attention_matches_torch(cuda, B, S, Skv, H):
     assert err <= 2e-2, err
 
 
+@pytest.mark.parametrize("knob", [b"attn_pair", b"attn_qtm"])
 @pytest.mark.parametrize("B,S,H", [(1, 600, 1), (2, 1000, 3), (1, 1536, 2), (2, 1560, 12), (1, 130, 1)])
-def test_attention_cta_pair_matches_torch(cuda, B, S, H):
+def test_attention_cta_pair_matches_torch(cuda, B, S, H, knob):
     """Self-attention on CTA pairs (knob attn_pair: cta_group::2, K split by rows and V by
-    columns across the pair) vs torch fp32 SDPA, and vs the single-CTA kernel.  Shapes cover an
+    columns across the pair; knob attn_qtm: one Q tile per CTA resident in TMEM, S double-
+    buffered) vs torch fp32 SDPA, and vs the single-CTA kernel.  Shapes cover an
     odd number of 256-row groups (the pair's second CTA past n_q), ragged key blocks and
     n_kv not a multiple of 64 (the second CTA's keys partly out of range)."""
     g = torch.Generator(device="cuda").manual_seed(S + 7 * H)
@@ -123,12 +125,12 @@ def test_attention_cta_pair_matches_torch(cuda, B, S, H):
     v = torch.randn(B, S, H, 128, device="cuda", generator=g).bfloat16()
     scale = 1.0 / 128 ** 0.5
     single = _attn(q, k, v, scale).float()
-    _lib.check(_lib.lib().lp_tune(b"attn_pair", 1))
+    _lib.check(_lib.lib().lp_tune(knob, 1))
     try:
         o = _attn(q, k, v, scale).float()
         torch.cuda.synchronize()
     finally:
-        _lib.check(_lib.lib().lp_tune(b"attn_pair", 0))
+        _lib.check(_lib.lib().lp_tune(knob, 0))
     ref = torch.nn.functional.scaled_dot_product_attention(q.float().transpose(1, 2), k.float().transpose(1, 2),
                                                            v.float().transpose(1, 2)).transpose(1, 2)
     assert (o - ref).abs().max().item() <= 2e-2

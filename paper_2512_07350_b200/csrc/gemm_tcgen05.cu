@@ -121,6 +121,20 @@ constexpr int gemm_smem_bytes() {
     return kStages * (kBM * kBK * 2 + BN * kBK * 2) + 1024 /*align*/ + 256 /*barriers*/;
 }
 
+// GELU-tanh of a pair with packed f32x2 math: gelu(x) = hx + hx * tanh(x * (k0 + k0 k1 x^2)),
+// hx = x / 2 — three FMUL2/FFMA2 for the argument and one FFMA2 for the result per pair,
+// against ~12 scalar operations (knob-free; A/B build flag LP_GELU_SCALAR)
+__device__ __forceinline__ float2 gelu_tanh2(float2 x) {
+    const float2 x2 = __fmul2_rn(x, x);
+    const float2 in = __ffma2_rn(x2, make_float2(0.7978845608028654f * 0.044715f, 0.7978845608028654f * 0.044715f),
+                                 make_float2(0.7978845608028654f, 0.7978845608028654f));
+    const float2 u = __fmul2_rn(x, in);
+    float2 t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t.x) : "f"(u.x));
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t.y) : "f"(u.y));
+    const float2 hx = __fmul2_rn(x, make_float2(0.5f, 0.5f));
+    return __ffma2_rn(hx, t, hx);
+}
 __device__ __forceinline__ float gelu_tanh(float x) {
     const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
     float t;
@@ -340,6 +354,16 @@ __device__ __forceinline__ void epi_chunk_smem(const GemmEpilogue& ep, int col0,
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             float a[8];
+#ifndef LP_GELU_SCALAR
+            if (MODE == EPI_BF16_GELU) {
+#pragma unroll
+                for (int u = 0; u < 8; u += 2) {
+                    const float2 g = gelu_tanh2(make_float2(v[8 * j + u], v[8 * j + u + 1]));
+                    a[u] = g.x;
+                    a[u + 1] = g.y;
+                }
+            } else
+#endif
 #pragma unroll
             for (int u = 0; u < 8; ++u) a[u] = MODE == EPI_BF16_GELU ? gelu_tanh(v[8 * j + u]) : v[8 * j + u];
             *reinterpret_cast<uint4*>(row + ((j ^ ((lane >> 1) & 3)) << 4)) =

@@ -136,6 +136,8 @@ class Cfg:
             "parallelism": f"lp{self.K} over {world} GPU(s)" if self.M == 1 else
             f"hybrid: {world // self.M} LP groups x {self.M} pipeline stages",
             "l2": "working set > L2 (2.6 GB of bf16 weights streamed per forward, >100 MB activations)",
+            "cuda_graphs": "each step graph captured before the warm-up (priming steps on a scratch copy of z, "
+                           "restored after); warm-up and timed steps replay graphs",
         }
 
 
@@ -450,7 +452,20 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # warm-up (every axis's graph is captured on its second occurrence)
+    # One-time setup, outside every timed region: the engine captures each step graph (one per
+    # schedule axis, and per exchange-buffer parity on the peer path) on that graph's second
+    # occurrence.  Run those occurrences now on a scratch copy of the latent, so the W warm-up
+    # steps and the K timed steps replay captured graphs (otherwise the first cycle of timed
+    # steps would include the eager runs and graph instantiation).
+    n_graph_keys = len(cfg.axes()) * (2 if exchange == "peer" else 1)
+    z_keep = eng.z.data.clone()
+    for s in range(1, 2 * n_graph_keys + 1):
+        eng.run(step_index(s), 1)
+    eng.sync(tmo)
+    eng.z.data.copy_(z_keep)
+    del z_keep
+
+    # warm-up
     for s in range(1, args.warmup + 1):
         eng.run(step_index(s), 1)
     eng.sync(tmo)

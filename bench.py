@@ -706,6 +706,37 @@ def self_launch(args):
         raise SystemExit(f"bench.py --gpus {n}: a rank failed (torchrun exit {r.returncode})")
 
 
+def run_guarded(args):
+    """N = 1: run the measurement in a child process (same arguments) and retry it once if it
+    stalls or fails, printing the child's JSON line.  Two stalls were seen in ~60 runs of this
+    round's A/B loops (both in runs of the default kernels, neither reproduced in 36 watched
+    runs, profiles/r4r); a stalled CUDA context cannot be recovered in-process, so the guard
+    restarts the whole measurement.  A retried line carries "attempts": 2."""
+    import signal
+
+    budget = args.attempt_timeout or (600 if args.config == "c2" else 3000)
+    env = dict(os.environ, LP_BENCH_CHILD="1")
+    for attempt in (1, 2):
+        p = subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], stdout=subprocess.PIPE,
+                             env=env, start_new_session=True)
+        try:
+            out, _ = p.communicate(timeout=budget)
+        except subprocess.TimeoutExpired:
+            os.killpg(p.pid, signal.SIGKILL)
+            p.wait()
+            print(f"bench.py: attempt {attempt} stalled ({budget} s)", file=sys.stderr, flush=True)
+            continue
+        lines = [x for x in out.decode().splitlines() if x.strip()]
+        if p.returncode == 0 and lines:
+            line = json.loads(lines[-1])
+            if attempt > 1:
+                line["attempts"] = attempt
+            print(json.dumps(line), flush=True)
+            return
+        print(f"bench.py: attempt {attempt} failed (exit {p.returncode})", file=sys.stderr, flush=True)
+    raise SystemExit("bench.py: the measurement failed twice")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -731,7 +762,13 @@ def main():
     ap.add_argument("--hbm-sets", type=int, default=8, help="buffer copies the K1/K10 replays cycle through")
     ap.add_argument("--sync-timeout", type=float, default=600.0, help="seconds before a stalled step is a WorkerFailure")
     ap.add_argument("--plan-only", action="store_true", help="print the N-rank assignment and FLOP-ideal bound (no GPU)")
+    ap.add_argument("--attempt-timeout", type=float, default=0.0,
+                    help="N = 1: seconds before a stalled measurement is restarted (default 600 for c2, 3000 otherwise)")
     args = ap.parse_args()
+    if ("WORLD_SIZE" not in os.environ and args.gpus == 1 and args.impl == "ours" and not args.plan_only
+            and not os.environ.get("LP_BENCH_CHILD")):
+        run_guarded(args)
+        return
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         self_launch(args)
         return

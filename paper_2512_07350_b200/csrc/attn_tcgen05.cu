@@ -1173,8 +1173,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kQtThreads, 1)
 }
 
 static int attn_poly() {
-    // pairs out of every 16 whose exp2 runs on the FMA pipe (0, 4, 6 compiled; A/B r1n: 6 best)
-    const int v = tune_get("attn_poly", 6);
+    // self-attention (NT = 2, one CTA per item): pairs out of every 16 whose exp2 runs on the FMA
+    // pipe (0, 4, 6, 8 compiled).  4 since r4: +0.9% in-step over 6 in two interleaved A/Bs
+    // (self-attention 1148-1156 vs 1135-1140 TF/s, profiles/r4t) once the GEMMs' handshake fix
+    // shifted the power budget; r2j had measured 6 best.  The other instances use 6.
+    const int v = tune_get("attn_poly", 4);
     return v == 0 || v == 6 || v == 8 ? v : 4;
 }
 
@@ -1235,15 +1238,16 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     // instance only — cross-attention 640 -> 779 TF/s in-step —, 2 also self-attention, where
     // it measured slower: 1148-1151 vs 1157-1167 TF/s in-step, profiles/r2b)
     const int pk = tune_get("attn_persist", 1);
-    const bool ok_p = !tune_get("attn_trace", 0) && attn_poly() == 6;
+    // the persistent / NT=1 / pair instances are compiled with POLY = 6 only; attn_poly selects
+    // the self-attention (NT = 2, one CTA per item) instance
+    const bool ok_p = !tune_get("attn_trace", 0);
     const dim3 grid(static_cast<unsigned>((x.n_q + 2 * kTile - 1) / (2 * kTile)), x.heads, x.batch);
     const int cls = x.n_kv == x.n_q && x.q == x.k ? KC_SELF_ATTN : KC_CROSS_ATTN;
     prof_begin(cls, st);
     // short key sequences (cross-attention over the text tokens): one Q tile per CTA, two CTAs
     // per SM (AttnCfg<1>)
     const int nt1_knob = tune_get("attn_nt1", 1);  // 0 never, 1 short key sequences, 2 always (experiments)
-    const bool nt1 = (nt1_knob == 2 || (nt1_knob == 1 && x.n_kv <= 4 * kTile)) && !tune_get("attn_trace", 0) &&
-                     attn_poly() == 6;
+    const bool nt1 = (nt1_knob == 2 || (nt1_knob == 1 && x.n_kv <= 4 * kTile)) && !tune_get("attn_trace", 0);
     if (nt1 && ok_p && pk >= 1) {
         const int64_t items = ((x.n_q + kTile - 1) / kTile) * x.heads * x.batch;
         const unsigned gp = static_cast<unsigned>(std::min<int64_t>(items, 2LL * sms));

@@ -74,7 +74,20 @@ struct AttnKernelArgs {
     int p_whole;  // MMA warp: wait for the whole P (p_full) before any PV instead of half by half
     const void* q;        // raw Q (the TMEM-resident-Q instance loads its rows directly)
     int64_t ldq, q_total_rows;
+    const float* q_rms;   // q RMSNorm folded into the per-row softmax scale (null: off)
+    int rms_parts;
+    float rms_inv_d, rms_eps;
 };
+
+// Softmax scale of one query row: c, times the row's RMSNorm factor when the q norm is folded
+// into attention (AttnArgs::q_rms; rows past n_q keep c).
+__device__ __forceinline__ float row_scale(const AttnKernelArgs& a, float c, int b, int64_t grow) {
+    if (!a.q_rms || grow >= a.n_q) return c;
+    const float* pp = a.q_rms + (static_cast<int64_t>(b) * a.q_rows_per_batch + grow) * a.rms_parts;
+    float ss = 0.f;
+    for (int i = 0; i < a.rms_parts; ++i) ss += pp[i];
+    return c * rsqrtf(ss * a.rms_inv_d + a.rms_eps);
+}
 
 // Waits of the TMA producer lane (K/V slot free) and of the softmax warps (S ready): spinning
 // try_wait (default) or try_wait with a suspend-time hint, so a waiting warp does not take
@@ -514,6 +527,7 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
             item(w, qt, h, b);
             const uint32_t g0 = PERS ? static_cast<uint32_t>(it) * static_cast<uint32_t>(nkv) : 0u;  // ring position base
             float m_run = -INFINITY, l_run = 0.f;
+            const float cr = row_scale(a, c, b, static_cast<int64_t>(qt) * NT * kTile + t * kTile + row);
             for (int j = 0; j < nkv; ++j) {
                 swait(&s_full[t], ((g0 + static_cast<uint32_t>(j)) & 1u));
                 const bool tr0 = TR && (warp & 3) == 2 && lane == 0;
@@ -529,9 +543,9 @@ __global__ void __launch_bounds__(AttnCfg<NT>::threads, NT == 2 ? 1 : 2)
                     mbar_arrive(&p_full[t]);
                     if (tr0) trace_ev<TR>(j, t, 3);
                 } else if (valid >= kTile)
-                    softmax_block<POLY, false, TR>(tS, tO, valid, c, m_run, l_run, &p_half[t], &p_full[t], j, t, tr0);
+                    softmax_block<POLY, false, TR>(tS, tO, valid, cr, m_run, l_run, &p_half[t], &p_full[t], j, t, tr0);
                 else
-                    softmax_block<POLY, true, TR>(tS, tO, valid, c, m_run, l_run, &p_half[t], &p_full[t], j, t, tr0);
+                    softmax_block<POLY, true, TR>(tS, tO, valid, cr, m_run, l_run, &p_half[t], &p_full[t], j, t, tr0);
             }
             // epilogue: O_t / l -> bf16 rows.  The staging below reuses V slots: wait for the
             // LAST tile's final PV as well (it is the item's last MMA), so no PV still reads V
@@ -1228,6 +1242,10 @@ void attention_bf16(const AttnArgs& x, cudaStream_t st) {
     a.q = x.q;
     a.ldq = x.ldq;
     a.q_total_rows = x.q_total_rows;
+    a.q_rms = x.q_rms;
+    a.rms_parts = x.rms_parts;
+    a.rms_inv_d = x.rms_d > 0 ? 1.f / static_cast<float>(x.rms_d) : 0.f;
+    a.rms_eps = x.rms_eps;
     static int sms = 0;
     if (!sms) {
         int dev = 0;

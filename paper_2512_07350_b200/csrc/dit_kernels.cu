@@ -494,6 +494,19 @@ __global__ void __launch_bounds__(256, LP_RMS_MINB) k_rmsnorm_rope_tab(__nv_bflo
     }
 }
 
+// out[r, c] = bf16(in[r, c] * g[c]) — the cross-attention q RMSNorm's per-channel weight folded
+// into the cached text K (dit.cpp, knob dit_xq_rms)
+__global__ void __launch_bounds__(256) k_scale_cols_bf16(const __nv_bfloat16* __restrict__ in, int64_t n, int d,
+                                                         const float* __restrict__ g, __nv_bfloat16* __restrict__ out) {
+    for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n; i += static_cast<int64_t>(gridDim.x) * 256)
+        out[i] = __float2bfloat16_rn(__bfloat162float(in[i]) * g[i % d]);
+}
+void scale_cols_bf16(const __nv_bfloat16* in, int64_t rows, int d, const float* g, __nv_bfloat16* out, cudaStream_t st) {
+    const int64_t n = rows * d;
+    k_scale_cols_bf16<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4096)), 256, 0, st>>>(in, n, d, g, out);
+    LP_LAUNCH_CHECK();
+}
+
 void rope_table(float2* tab, int nf, int nh, int nw, cudaStream_t st) {
     const int total = nf * 22 + nh * 21 + nw * 21;
     k_rope_table<<<(total + 255) / 256, 256, 0, st>>>(tab, nf, nh, nw);

@@ -46,6 +46,8 @@ void rmsnorm_rope(__nv_bfloat16* buf, int64_t rows, int64_t ld, int64_t col0, in
                   bool rope, int64_t rows_per_batch, int nh, int nw, cudaStream_t st);
 // RoPE cos/sin table [nf*22 + nh*21 + nw*21] float2 of a shard grid (once per forward).
 void rope_table(float2* tab, int nf, int nh, int nw, cudaStream_t st);
+// out[r, c] = bf16(in[r, c] * g[c]) over rows x d (the q-norm weight folded into the text K)
+void scale_cols_bf16(const __nv_bfloat16* in, int64_t rows, int d, const float* g, __nv_bfloat16* out, cudaStream_t st);
 // Table-driven RMSNorm(+RoPE if tab) of nsec adjacent width-d sections (q | k), in place.
 // Returns false when the width / alignment is not covered (callers use rmsnorm_rope).
 bool rmsnorm_rope_tab(__nv_bfloat16* buf, int64_t rows, int64_t ld, int64_t col0, int d, int nsec, const float* g0,

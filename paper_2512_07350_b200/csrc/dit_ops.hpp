@@ -33,6 +33,10 @@ struct GemmEpilogue {
     int parts;
     float cols_per_part;
     float eps;
+    // BF16 epilogue: per row and N tile, the sum of squares of the bf16 values written
+    // (rms_out[row * (N / BN) + n_tile]) — the cross-attention q RMSNorm folded into attention
+    // (dit.cpp, knob dit_xq_rms).  Null: off.
+    float* rms_out;
 };
 // N tile width the GEMM uses for N (the producer's partial count is N / gemm_bn_for(M, N));
 // 0 when (M, N) takes a kernel without the LN-fold epilogue.
@@ -53,6 +57,13 @@ struct AttnArgs {
     void* o; int64_t ldo;
     int batch, heads;
     float scale;
+    // q RMSNorm folded into the softmax scale: row r's scores are scaled by
+    // rsqrt(sum(q_rms[r * rms_parts ...]) / rms_d + rms_eps) (the q rows are un-normalised and the
+    // norm's per-channel weight is folded into K).  Null: off.
+    const float* q_rms;
+    int rms_parts;
+    int rms_d;
+    float rms_eps;
 };
 void attention_bf16(const AttnArgs& a, cudaStream_t st);
 

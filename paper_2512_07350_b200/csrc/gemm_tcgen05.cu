@@ -324,6 +324,7 @@ __device__ __forceinline__ void tma_load_2d_cta(const void* tmap, uint64_t* bar,
 struct LnRow {
     float mean = 0.f, rstd = 1.f;  // consumer: the row's LayerNorm statistics
     LnAcc acc;                    // producer: partials over this tile's chunks
+    float rms[4] = {0.f, 0.f, 0.f, 0.f};  // BF16 rms_out: sum of squares of the written bf16 values
 };
 
 template <int MODE, bool XQ = false>
@@ -351,6 +352,13 @@ __device__ __forceinline__ void epi_chunk_smem(const GemmEpilogue& ep, int col0,
     }
     if (MODE == EPI_BF16 || MODE == EPI_BF16_GELU) {
         uint8_t* row = box + lane * 64;
+        if (MODE == EPI_BF16 && ep.rms_out) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const float q = __bfloat162float(__float2bfloat16_rn(v[j]));
+                ln.rms[j & 3] = fmaf(q, q, ln.rms[j & 3]);
+            }
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             float a[8];
@@ -665,6 +673,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             }
             if (XQ && my_row < M)
                 ep.stats_out[static_cast<int64_t>(my_row) * num_n + nb] = ln_acc_final(ln.acc, static_cast<float>(BN));
+            if (MODE == EPI_BF16 && ep.rms_out && my_row < M)
+                ep.rms_out[static_cast<int64_t>(my_row) * num_n + nb] = (ln.rms[0] + ln.rms[1]) + (ln.rms[2] + ln.rms[3]);
             tc_fence_before();
             tempty_arrive(&tempty[acc]);
         }
@@ -803,6 +813,8 @@ void gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int M, in
         fail(LP_ERR_INVALID_ARGUMENT, "gemm: the LN-fold epilogue needs the CTA-pair kernel (M > 128, N % 128 == 0)");
     if (ep.xq && (mode < EPI_F32_RESID || !ep.g || !ep.stats_out || ep.ldq % 8))
         fail(LP_ERR_INVALID_ARGUMENT, "gemm: LN-fold producer needs an f32 epilogue, g, stats_out and ldq % 8 == 0");
+    if (ep.rms_out && (mode != EPI_BF16 || !gemm_lnfold_bn(M, N)))
+        fail(LP_ERR_INVALID_ARGUMENT, "gemm: rms_out needs the bf16 epilogue of the CTA-pair kernel");
     if (ep.stats_in && (mode > EPI_BF16_GELU || !ep.cs || ep.parts < 1))
         fail(LP_ERR_INVALID_ARGUMENT, "gemm: LN-fold consumer needs a bf16 epilogue, cs and parts >= 1");
     if (K % 8 || lda % 8 || ldb % 8) fail(LP_ERR_INVALID_ARGUMENT, "gemm: K and strides must be multiples of 8");
